@@ -1,0 +1,145 @@
+/*
+ * kvp_b200.h — C-ABI of the B200-native AttentionPack KV-cache path.
+ *
+ * This is the drop-in boundary.  Every entry point takes plain pointers,
+ * sizes and POD descriptors (no C++ or torch types), returns an int status,
+ * never throws, and leaves a thread-local message behind on failure:
+ *
+ *   0 KVP_OK            1 KVP_ERR_PARAMETER   (kvpack::parameter_error)
+ *   2 KVP_ERR_SHAPE     (kvpack::shape_error) 3 KVP_ERR_DATA (kvpack::data_error)
+ *   4 KVP_ERR_IO        (kvpack::io_error)    5 KVP_ERR_CUDA (device failure)
+ *
+ * The codes map 1:1 onto the reference's exception hierarchy
+ * (/root/reference/proj/include/kvpack/errors.hpp:11-36); the C++ facade
+ * and the Python layer turn them back into the same exception types
+ * (bindings/module.cpp:117-127: io -> OSError, parameter/shape/data -> ValueError).
+ *
+ * Streams are caller-owned (`stream` is a cudaStream_t passed as void*;
+ * NULL = legacy default stream).  Device pointers are marked [dev], host
+ * pointers [host].  A kvp_ctx is single-writer, like a reference LayerCache
+ * (SPEC.md:151).
+ *
+ * Which reference interface each entry point replaces is cited beside it.
+ */
+#ifndef KVP_B200_H
+#define KVP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KVP_ABI_VERSION 1
+
+enum kvp_status {
+  KVP_OK = 0,
+  KVP_ERR_PARAMETER = 1,
+  KVP_ERR_SHAPE = 2,
+  KVP_ERR_DATA = 3,
+  KVP_ERR_IO = 4,
+  KVP_ERR_CUDA = 5
+};
+
+/* Storage precision of cache payloads (the reference instantiates float and
+ * double, cache.cpp:241-242; bf16 is the B200 serving format). */
+enum kvp_dtype { KVP_F32 = 0, KVP_F64 = 1, KVP_BF16 = 2 };
+
+/* Store forms (cache.hpp:35-60 BlockStore): dense rows or low-rank factors. */
+enum kvp_form { KVP_DENSE = 0, KVP_LOWRANK = 1 };
+
+int kvp_abi_version(void);
+const char* kvp_last_error_message(void);
+/* Number of CUDA kernel launches issued by this library so far (process-wide). */
+uint64_t kvp_launch_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* Retrieval-plan attention (generic path, any dtype, any plan).             */
+/* ------------------------------------------------------------------------ */
+
+/* One stored matrix.  KVP_DENSE: a = rows (n x width, row stride lda).
+ * KVP_LOWRANK: a = left (n x rank, stride lda), b = right (rank x width,
+ * stride ldb).  [dev] pointers in `dtype`. */
+typedef struct {
+  int32_t form;
+  int32_t rank;
+  const void* a;
+  const void* b;
+  int64_t lda;
+  int64_t ldb;
+} kvp_store;
+
+/* One RetrievalPlan entry (decoder.hpp:84-98): which K/V stores the row
+ * comes from, the row inside them, the tier rank prefixes (0 = full stored
+ * rank / dense), the global position (causal visibility), and the column of
+ * the importance table it maps to (decoder.cpp:596-600; -1 = none). */
+typedef struct {
+  int32_t k_store;
+  int32_t v_store;
+  uint32_t row;
+  uint32_t rank_k;
+  uint32_t rank_v;
+  int32_t table_index;
+  uint64_t position;
+} kvp_plan_entry;
+
+typedef struct {
+  int32_t heads;      /* H   (HeadGeometry, cache.hpp:21-31) */
+  int32_t kv_heads;   /* H_kv */
+  int32_t head_dim;   /* D */
+  int32_t dtype;      /* kvp_dtype of every store */
+  int32_t n_stores;
+  int32_t n_entries;
+  int32_t tq;         /* query rows */
+  int32_t table_size; /* importance-table width for head_avg_table (0 = skip) */
+  const kvp_store* stores;          /* [host] n_stores */
+  const kvp_plan_entry* entries;    /* [host] n_entries, plan order */
+  const double* queries;            /* [dev] tq x H*D */
+  const uint64_t* query_positions;  /* [dev] tq */
+  double* context;                  /* [dev] out tq x H*D (pre-W_o) */
+  double* head_avg;                 /* [dev] out tq x n_entries, plan order (nullable) */
+  double* head_avg_table;           /* [dev] out tq x table_size, table order (nullable) */
+} kvp_attend_desc;
+
+/* attend_materialized / attend_fused (decoder.hpp:127-135, decoder.cpp:190-344)
+ * evaluated in the low-rank space: P = right_k·q, S = left_k·P, softmax,
+ * U = p·left_v, out = U·right_v — never rebuilding K~/V~.  fp64 accumulation
+ * (the reference accumulates in double for both T=float and T=double). */
+int kvp_attend_plan(const kvp_attend_desc* desc, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* Importance (importance.cpp:33-117).                                       */
+/* ------------------------------------------------------------------------ */
+
+/* EMA update of `n_tables` tables of `n` scores each (importance.cpp:33-65):
+ * s <- decay*s + blend*mean_t attn[t, :], decay = alpha^tq (computed on the
+ * host with std::pow like the reference), bit-exact (no FMA contraction).
+ * Rows must be distributions within 1e-4 (else KVP_ERR_DATA after the sync
+ * when `check` != 0; *bad_rows receives the count when non-NULL). */
+int kvp_update_importance(int32_t n_tables, int32_t n, double* scores /*[dev] n_tables x n*/,
+                          int32_t tq, const double* attn /*[dev] n_tables x tq x n*/,
+                          double alpha, int32_t check, void* stream);
+
+/* Tier assignment (importance.cpp:67-117 assign_groups + decoder.cpp:105-139
+ * resolve_tiering): per table, stable order by (score desc, index asc) of the
+ * n compressed tokens; group f gets floor(ratio_f*n+0.5) tokens (last takes
+ * the rest).  Outputs the group id per token and the per-token rank prefixes
+ * rank_k[f], rank_v[f].  Bit-exact vs the reference for identical scores. */
+int kvp_assign_tiers(int32_t n_tables, int32_t n, const double* scores /*[dev] stride score_stride*/,
+                     int64_t score_stride, int32_t n_groups, const double* ratios /*[host]*/,
+                     const int32_t* key_ranks /*[host]*/, const int32_t* value_ranks /*[host]*/,
+                     uint8_t* tier_out /*[dev] n_tables x n (nullable)*/,
+                     uint16_t* rank_k_out /*[dev] n_tables x n (nullable)*/,
+                     uint16_t* rank_v_out /*[dev] n_tables x n (nullable)*/, void* stream);
+
+/* Host-buffer convenience forms used by the kvpack-compatible Python surface
+ * (bindings/module.cpp:186-225 ema_update / assign_groups). */
+int kvp_update_importance_host(int32_t n, double* scores, int32_t tq, const double* attn, double alpha);
+int kvp_assign_groups_host(int32_t n, const double* scores, int32_t n_groups, const double* ratios,
+                           const int32_t* ranks, uint32_t* tier_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVP_B200_H */

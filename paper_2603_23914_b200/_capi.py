@@ -1,0 +1,112 @@
+"""ctypes binding of the C-ABI in include/kvp_b200.h (libkvp_b200.so).
+
+The product path: every call lands in hand-written sm_100a kernels.  There is
+no CPU fallback — if the shared library is missing the import fails loudly.
+Status codes become the exception types the reference's Python module raises
+(bindings/module.cpp:117-127): io -> OSError, parameter/shape/data -> ValueError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libkvp_b200.so"
+
+KVP_OK, KVP_ERR_PARAMETER, KVP_ERR_SHAPE, KVP_ERR_DATA, KVP_ERR_IO, KVP_ERR_CUDA = range(6)
+KVP_F32, KVP_F64, KVP_BF16 = 0, 1, 2
+KVP_DENSE, KVP_LOWRANK = 0, 1
+
+
+class KvpError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+class KvpParameterError(KvpError, ValueError):
+    pass
+
+
+class KvpShapeError(KvpParameterError):
+    pass
+
+
+class KvpDataError(KvpError, ValueError):
+    pass
+
+
+class KvpIOError(KvpError, OSError):
+    pass
+
+
+class KvpCudaError(KvpError):
+    pass
+
+
+_ERRORS = {KVP_ERR_PARAMETER: KvpParameterError, KVP_ERR_SHAPE: KvpShapeError, KVP_ERR_DATA: KvpDataError,
+           KVP_ERR_IO: KvpIOError, KVP_ERR_CUDA: KvpCudaError}
+
+
+class Store(C.Structure):
+    _fields_ = [("form", C.c_int32), ("rank", C.c_int32), ("a", C.c_void_p), ("b", C.c_void_p),
+                ("lda", C.c_int64), ("ldb", C.c_int64)]
+
+
+class PlanEntry(C.Structure):
+    _fields_ = [("k_store", C.c_int32), ("v_store", C.c_int32), ("row", C.c_uint32), ("rank_k", C.c_uint32),
+                ("rank_v", C.c_uint32), ("table_index", C.c_int32), ("position", C.c_uint64)]
+
+
+class AttendDesc(C.Structure):
+    _fields_ = [("heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("dtype", C.c_int32),
+                ("n_stores", C.c_int32), ("n_entries", C.c_int32), ("tq", C.c_int32), ("table_size", C.c_int32),
+                ("stores", C.POINTER(Store)), ("entries", C.POINTER(PlanEntry)), ("queries", C.c_void_p),
+                ("query_positions", C.c_void_p), ("context", C.c_void_p), ("head_avg", C.c_void_p),
+                ("head_avg_table", C.c_void_p)]
+
+
+# name -> (restype, argtypes); every symbol include/kvp_b200.h declares.
+SIGNATURES = {
+    "kvp_abi_version": (C.c_int, []),
+    "kvp_last_error_message": (C.c_char_p, []),
+    "kvp_launch_count": (C.c_uint64, []),
+    "kvp_attend_plan": (C.c_int, [C.POINTER(AttendDesc), C.c_void_p]),
+    "kvp_update_importance": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_double,
+                                        C.c_int32, C.c_void_p]),
+    "kvp_assign_tiers": (C.c_int, [C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "kvp_update_importance_host": (C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_double]),
+    "kvp_assign_groups_host": (C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+}
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} is missing — build it with `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (no CPU fallback exists)")
+        l = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(l, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = l
+    return _lib
+
+
+def check(rc: int):
+    if rc != KVP_OK:
+        msg = lib().kvp_last_error_message().decode()
+        raise _ERRORS.get(rc, KvpError)(rc, msg)
+
+
+def call(name, *args):
+    check(getattr(lib(), name)(*args))
+
+
+def launch_count() -> int:
+    return int(lib().kvp_launch_count())
