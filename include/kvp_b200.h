@@ -139,6 +139,46 @@ int kvp_update_importance_host(int32_t n, double* scores, int32_t tq, const doub
 int kvp_assign_groups_host(int32_t n, const double* scores, int32_t n_groups, const double* ratios,
                            const int32_t* ranks, uint32_t* tier_out);
 
+/* ------------------------------------------------------------------------ */
+/* Fused serving kernel: bf16 compressed cache, T_q = 1, batched instances.  */
+/* ------------------------------------------------------------------------ */
+
+/* One layer of a batch of caches in the serving layout: every instance holds
+ * one factored block of n_comp tokens (left_k/left_v: [batch][n_comp][ld_left],
+ * right_k: [batch][rank_k][W], right_v: [batch][rank_v][W]) and a dense tail
+ * (tail_k/tail_v: [batch][tail_cap][W], n_tail rows valid — read from
+ * n_tail_dev when non-NULL so the call can live in a CUDA graph).  This is
+ * the plan build_retrieval_plan produces for the reference's default
+ * configuration (visual block factored, textual tail dense; decoder.cpp:141-188)
+ * with untiered decompression.  Outputs the pre-W_o context (decoder.cpp:587-590)
+ * and, when `importance` is set, applies the Eq. 1 EMA in place for T_q = 1
+ * (importance.cpp:33-65) over [compressed..., tail...] columns. */
+typedef struct {
+  int32_t heads, kv_heads, head_dim, batch;
+  int32_t n_comp, rank_k, rank_v, ld_left;
+  int32_t tail_cap, n_tail;
+  const int32_t* n_tail_dev;    /* [dev] nullable */
+  int32_t cluster;              /* CTAs per instance, 0 = auto */
+  int32_t context_bf16;         /* 1: context is bf16, 0: fp32 */
+  const void* left_k;           /* [dev] bf16 */
+  const void* right_k;
+  const void* left_v;
+  const void* right_v;
+  const void* tail_k;
+  const void* tail_v;
+  const float* queries;         /* [dev] batch x H*D (unscaled) */
+  double* importance;           /* [dev] batch x imp_stride, nullable */
+  int64_t imp_stride;
+  double alpha;
+  float* head_avg;              /* [dev] batch x (n_comp + tail_cap), nullable */
+  void* context;                /* [dev] batch x H*D */
+} kvp_fused_desc;
+
+/* decode_step's attention + importance for a whole batch (decoder.cpp:583-601)
+ * as one cluster launch.  KVP_ERR_PARAMETER when the shape is outside the
+ * fused kernel's envelope (then use kvp_attend_plan). */
+int kvp_decode_fused(const kvp_fused_desc* desc, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

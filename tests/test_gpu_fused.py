@@ -1,0 +1,129 @@
+"""GPU parity of the fused cluster/tcgen05 decode kernel (kvp_decode_fused).
+
+Oracle: fp64 dense attention over K~ = [left_k right_k ; tail_k] and
+V~ = [left_v right_v ; tail_v] built from the *same bf16-rounded* factors
+(SURVEY.md §8c parity protocol: identical rounded inputs, bf16 bound 1e-3),
+plus the reference EMA (importance.cpp:33-65) on the head-averaged rows."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _torch():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+class FusedDesc(C.Structure):
+    _fields_ = [("heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("batch", C.c_int32),
+                ("n_comp", C.c_int32), ("rank_k", C.c_int32), ("rank_v", C.c_int32), ("ld_left", C.c_int32),
+                ("tail_cap", C.c_int32), ("n_tail", C.c_int32), ("n_tail_dev", C.c_void_p),
+                ("cluster", C.c_int32), ("context_bf16", C.c_int32),
+                ("left_k", C.c_void_p), ("right_k", C.c_void_p), ("left_v", C.c_void_p), ("right_v", C.c_void_p),
+                ("tail_k", C.c_void_p), ("tail_v", C.c_void_p), ("queries", C.c_void_p),
+                ("importance", C.c_void_p), ("imp_stride", C.c_int64), ("alpha", C.c_double),
+                ("head_avg", C.c_void_p), ("context", C.c_void_p)]
+
+
+def bf16_round(x):
+    torch = _torch()
+    return torch.as_tensor(x, dtype=torch.float32).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+def make_case(rng, B, H, Hkv, D, n, rk, rv, nt, cap):
+    W = Hkv * D
+    def orth(r):
+        q, _ = np.linalg.qr(rng.standard_normal((W, r)))
+        return q.T
+    case = dict(
+        left_k=bf16_round(rng.standard_normal((B, n, rk)) * np.linspace(3, 0.3, rk)),
+        left_v=bf16_round(rng.standard_normal((B, n, rv)) * np.linspace(3, 0.3, rv)),
+        right_k=bf16_round(np.stack([orth(rk) for _ in range(B)])),
+        right_v=bf16_round(np.stack([orth(rv) for _ in range(B)])),
+        tail_k=bf16_round(rng.standard_normal((B, cap, W))),
+        tail_v=bf16_round(rng.standard_normal((B, cap, W))),
+        q=rng.standard_normal((B, H * D)).astype(np.float32).astype(np.float64) * 2.0,
+        imp=rng.uniform(0, 1, (B, n + cap)),
+    )
+    return case
+
+
+def oracle(case, H, Hkv, D, nt, alpha):
+    B, n, _ = case["left_k"].shape
+    per = H // Hkv
+    ctx = np.zeros((B, H * D))
+    ha = np.zeros((B, n + nt))
+    imp = case["imp"].copy()
+    for b in range(B):
+        K = np.concatenate([case["left_k"][b] @ case["right_k"][b], case["tail_k"][b, :nt]])
+        V = np.concatenate([case["left_v"][b] @ case["right_v"][b], case["tail_v"][b, :nt]])
+        for h in range(H):
+            g = h // per
+            s = K[:, g * D:(g + 1) * D] @ case["q"][b, h * D:(h + 1) * D] / np.sqrt(D)
+            e = np.exp(s - s.max())
+            z = e.sum()
+            ctx[b, h * D:(h + 1) * D] = e @ V[:, g * D:(g + 1) * D] / z
+            ha[b] += e / z / H
+        cols = np.r_[np.arange(n), n + np.arange(nt)]
+        imp[b, cols] = alpha * imp[b, cols] + (1 - alpha) * ha[b]
+    return ctx, ha, imp
+
+
+def run_fused(case, H, Hkv, D, nt, alpha, cluster=0, ld_pad=8):
+    torch = _torch()
+    from paper_2603_23914_b200 import _capi as capi
+    B, n, rk = case["left_k"].shape
+    rv = case["left_v"].shape[2]
+    cap = case["tail_k"].shape[1]
+    ld = ((max(rk, rv) + ld_pad - 1) // ld_pad) * ld_pad
+    def left(x):
+        out = torch.zeros((B, n, ld), dtype=torch.bfloat16)
+        out[:, :, :x.shape[2]] = torch.as_tensor(x)
+        return out.cuda()
+    bf = lambda x: torch.as_tensor(x).to(torch.bfloat16).cuda().contiguous()
+    t = dict(lk=left(case["left_k"]), lv=left(case["left_v"]), rk=bf(case["right_k"]), rv=bf(case["right_v"]),
+             tk=bf(case["tail_k"]), tv=bf(case["tail_v"]), q=torch.as_tensor(case["q"], dtype=torch.float32).cuda(),
+             imp=torch.as_tensor(case["imp"]).cuda().contiguous())
+    ctx = torch.zeros((B, H * D), dtype=torch.float32, device="cuda")
+    ha = torch.zeros((B, n + cap), dtype=torch.float32, device="cuda")
+    d = FusedDesc(H, Hkv, D, B, n, rk, rv, ld, cap, nt, None, cluster, 0, t["lk"].data_ptr(), t["rk"].data_ptr(),
+                  t["lv"].data_ptr(), t["rv"].data_ptr(), t["tk"].data_ptr(), t["tv"].data_ptr(), t["q"].data_ptr(),
+                  t["imp"].data_ptr(), n + cap, alpha, ha.data_ptr(), ctx.data_ptr())
+    capi.lib().kvp_decode_fused.argtypes = [C.POINTER(FusedDesc), C.c_void_p]
+    capi.check(capi.lib().kvp_decode_fused(C.byref(d), None))
+    torch.cuda.synchronize()
+    return ctx.cpu().numpy().astype(np.float64), ha.cpu().numpy().astype(np.float64), t["imp"].cpu().numpy()
+
+
+SHAPES = [
+    # B, H, Hkv, D, n_comp, rank_k, rank_v, n_tail, cap, cluster
+    (2, 32, 32, 128, 2304, 368, 368, 65, 320, 8),   # C2 geometry (4x compression), first decode step
+    (2, 40, 40, 128, 4096, 284, 284, 320, 320, 8),  # C3 geometry (8x), last decode step
+    (1, 32, 32, 128, 2048, 128, 128, 200, 320, 8),  # C5 geometry
+    (3, 8, 4, 64, 300, 40, 24, 5, 16, 8),           # GQA, ragged: idle CTAs, partial tiles, odd ranks
+    (2, 16, 16, 128, 1000, 100, 70, 0, 8, 4),       # no tail, cluster of 4
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_fused_matches_fp64_oracle(shape):
+    B, H, Hkv, D, n, rk, rv, nt, cap, cl = shape
+    rng = np.random.default_rng(hash(shape) % 2**32)
+    case = make_case(rng, B, H, Hkv, D, n, rk, rv, nt, cap)
+    alpha = 0.25
+    ctx, ha, imp = run_fused(case, H, Hkv, D, nt, alpha, cluster=cl)
+    rctx, rha, rimp = oracle(case, H, Hkv, D, nt, alpha)
+    scale = np.abs(rctx).max()
+    err = np.abs(ctx - rctx).max() / scale
+    assert err <= 1e-3, f"context rel err {err:.3e}"
+    cols = np.r_[np.arange(n), n + np.arange(nt)]
+    assert np.abs(ha[:, cols] - rha).max() <= 1e-4
+    assert np.allclose(ha[:, cols].sum(axis=1), 1.0, atol=1e-4)
+    assert np.abs(imp - rimp).max() <= 1e-4
+    untouched = np.setdiff1d(np.arange(n + cap), cols)
+    assert np.array_equal(imp[:, untouched], case["imp"][:, untouched])
