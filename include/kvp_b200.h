@@ -172,10 +172,18 @@ typedef struct {
   double alpha;
   float* head_avg;              /* [dev] batch x (n_comp + tail_cap), nullable */
   void* context;                /* [dev] batch x H*D */
+  void* workspace;              /* [dev] nullable: kvp_decode_fused_workspace() bytes */
+  size_t workspace_bytes;
 } kvp_fused_desc;
 
-/* decode_step's attention + importance for a whole batch (decoder.cpp:583-601)
- * as one cluster launch.  KVP_ERR_PARAMETER when the shape is outside the
+/* Bytes of device workspace kvp_decode_fused needs for `desc` (P, tail
+ * weights and U between its three launches); pass it to make the call
+ * allocation-free (and CUDA-graph capturable). */
+size_t kvp_decode_fused_workspace(const kvp_fused_desc* desc);
+
+/* decode_step's attention + importance for a whole batch (decoder.cpp:583-601):
+ * qdots (project q into the key basis + tail logits), the cluster/tcgen05
+ * low-rank core, and vsum (value basis multiply + tail values) — 3 launches.  KVP_ERR_PARAMETER when the shape is outside the
  * fused kernel's envelope (then use kvp_attend_plan). */
 int kvp_decode_fused(const kvp_fused_desc* desc, void* stream);
 

@@ -1,38 +1,40 @@
-// Fused decode attention over the compressed KV cache — one thread-block
-// cluster per (instance, layer), bf16 storage, tcgen05 tensor cores.
+// Compressed-cache decode attention, bf16 storage, T_q = 1 — the serving hot
+// path.  Replaces the reference's per-(instance, layer) decode loop
+// (decoder.cpp:555-601: build plan -> attend_{materialized,fused} ->
+// head-average -> update_importance), whose cost is ~100% row rebuilding in
+// store_decompress_row (cache.cpp:63-101).  Nothing of width W = H_kv*D is
+// rebuilt; every byte of the cache is read exactly once, in three launches:
 //
-// Replaces the reference's decode hot loop (decoder.cpp:555-601: build plan ->
-// attend_{materialized,fused} -> head-average -> update_importance), whose
-// cost is ~100% store_decompress_row (cache.cpp:63-101).  Nothing of width
-// W = H_kv*D is ever rebuilt; every byte of the cache is read once:
-//
-//   phase P  P[r,h]  = right_k[r, g(h)-slice] . q_h / sqrt(D)      CUDA cores, rows split over the cluster,
-//                                                                 slices exchanged through DSMEM
-//   phase S  S[t,h]  = left_k[t,:] . P[:,h]                         tcgen05, M=128 tokens, N=heads, K=rank,
-//                                                                 accumulators stay resident in TMEM
-//            tail    s[t,h] = tail_k[t, g-slice] . q_h / sqrt(D)     CUDA cores
-//   stats    cluster-wide max / normaliser per head via DSMEM (no online rescaling)
-//   phase U  U^T[r,h] += left_v[t,r] * p[t,h]   (r < rank_v(t))     tcgen05, M=128 ranks, N=heads, K=tokens
-//            tail    c[h,:] += p[t,h] * tail_v[t, g-slice]          CUDA cores
-//   output   out[h,:] = (sum_cluster U[h,:] . right_v[:, g-slice] + sum_cluster c[h,:]) / z_h
-//   EMA      importance[t] <- decay*imp + blend*mean_h p[t,h]/z_h  (importance.cpp:33-65), fp64
+//  1. qdots  (grid: kv-head x instance, CUDA cores, streaming)
+//       P[h, r]      = right_k[r, g(h)-slice] . q_h / sqrt(D)     (project q into the key basis)
+//       s_tail[h, t] = tail_k[t, g(h)-slice] . q_h / sqrt(D)     (dense-tail logits)
+//  2. core   (one thread-block cluster per instance, tcgen05 + TMEM + TMA + DSMEM)
+//       S[t, h]  = left_k[t, :] . P[h, :]        tcgen05 M=128 tokens, N=heads, K=rank; S stays in TMEM
+//       m_h, z_h over S and s_tail, reduced across the cluster through DSMEM (no online rescaling)
+//       p = exp(S - m);  importance EMA (importance.cpp:33-65) from the head average, fp64
+//       U^T[r, h] += left_v[t, r] p[t, h]         tcgen05 M=128 ranks, N=heads, K=tokens
+//       U (reduce-scattered over the cluster) / z_h -> workspace; p_tail / z_h -> workspace
+//  3. vsum   (grid: kv-head x instance, CUDA cores, streaming)
+//       out[h, :] = U[h, :] . right_v[:, g-slice] + p_tail[h, :] . tail_v[:, g-slice]
 //
 // bf16 operands: the cached factors are bf16 (the serving format); the
 // on-the-fly operands P and p are split into hi+lo bf16 pairs (two MMAs into
 // the same fp32 accumulator), so the only rounding vs an fp64 oracle fed the
 // same bf16 factors is fp32 accumulation.
 //
-// Warp roles (320 threads): warp 0 = TMA/bulk-copy producer, warp 1 = MMA
-// issuer + TMEM owner, warps 2..9 = compute (CUDA-core phases, TMEM
-// epilogues, DSMEM exchanges).  Every global byte the CTA consumes streams
-// through one 6-stage, 16 KB/stage mbarrier ring in a fixed item order that
-// producer and consumers derive identically.
+// core kernel warp roles (320 threads): warp 0 = TMA producer, warp 1 = MMA
+// issuer + TMEM owner, warps 2..9 = TMEM epilogues / softmax / EMA / DSMEM.
+// left_k / left_v stream through a 6-stage x 16 KB mbarrier ring in a fixed
+// item order that producer and MMA issuer derive identically.
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <map>
+#include <memory>
+#include <tuple>
 #include <string>
 
 #include "common.cuh"
@@ -49,11 +51,12 @@ constexpr uint32_t kStageBytes = 16384;
 constexpr int kThreads = 320;
 constexpr int kComputeThreads = 256;
 constexpr uint32_t kBarCompute = 1;  // named barrier id for the compute warps
-constexpr int kTailMax = 64;
+constexpr int kTailMax = 96;
+constexpr int kStreamThreads = 256;  // qdots / vsum blocks
 
 struct Smem {
-  uint32_t ring, phi, plo, pt, stail, part, stats, bars, tslot, total;
-  uint32_t uloc, ctxloc, ufin, tfin, red;  // late-phase aliases over [phi, stail)
+  uint32_t ring, phi, plo, pt, stail, part, stats, imps, bars, tslot, total;
+  uint32_t uloc;  // late-phase alias over [phi, ...), valid once the U MMAs completed
   int uloc_stride;
 };
 
@@ -66,20 +69,17 @@ __host__ __device__ inline Smem smem_layout(const FusedPlan& p) {
   s.phi = s.ring + kStages * kStageBytes;
   s.plo = s.phi + p.kpk * np * 128;
   s.pt = align_up(s.plo + p.kpk * np * 128, 1024);  // 2 buffers x {hi, lo} x 2 panels
-  s.stail = s.pt + 8 * np * 128;
-  s.part = s.stail + kTailMax * np * 4;
-  s.stats = s.part + 8 * np * 4 + 2 * 128 * 4;
-  s.bars = align_up(s.stats + 4 * np * 4, 8);
-  s.tslot = s.bars + 32 * 8;
-  s.total = align_up(s.tslot + 16, 1024);
-  // aliases, valid once the U MMAs have completed
+  const uint32_t pt_end = s.pt + 8 * np * 128;
   s.uloc_stride = static_cast<int>(align_up(p.s.rank_v, 4));
   s.uloc = s.phi;
-  s.ctxloc = s.uloc + np * s.uloc_stride * 4;
-  s.ufin = s.ctxloc + p.s.H * p.s.D * 4;
-  const int per_kv = p.s.H / p.s.Hkv;
-  s.tfin = s.ufin + p.heads_per_cta * per_kv * s.uloc_stride * 4;
-  s.red = s.tfin + p.heads_per_cta * per_kv * p.s.D * 4;
+  const uint32_t uloc_end = s.uloc + np * s.uloc_stride * 4;
+  s.stail = align_up(pt_end > uloc_end ? pt_end : uloc_end, 16);
+  s.part = s.stail + p.tail_max * np * 4;
+  s.stats = s.part + 16 * np * 4 + 2 * 128 * 4;
+  s.imps = align_up(s.stats + (5 + 8) * np * 4, 16);
+  s.bars = align_up(s.imps + (p.chunk + p.tail_max) * 8, 8);
+  s.tslot = s.bars + 32 * 8;
+  s.total = align_up(s.tslot + 16, 1024);
   return s;
 }
 
@@ -92,43 +92,39 @@ enum Bar : int {
   kPEmpty0, kPEmpty1,             // p tile buffer consumed (MMA -> compute)
   kUFull,                         // U MMAs complete
   kTmemFree,                      // compute finished reading TMEM
-  kSlices,                        // cluster: all P slices published (count C)
+  kSlices,                        // (unused)
   kStats,                         // cluster: all (m, z) published (count C)
-  kUReady,                        // cluster: all U / tail contexts published (count C)
+  kUReady,                        // cluster: all U partials published (count C)
   kDone,                          // cluster: all peers finished reading my smem (count C)
   kNumBars
 };
 
 struct Items {
-  int rk0, n_rk, tk0, n_tk, lk0, lv0, tv0, rv0, total;
-  int tiles, chunk_len, c_first, t_first, p_first;
-  int n_heads, nrb;
+  int lk0, lv0, total;
+  int n_tk, tiles, chunk_len, c_first, t_first;
 };
 
 __device__ __forceinline__ Items make_items(const FusedPlan& p, int c, int n_tail) {
   Items it{};
   const int C = p.s.cluster;
-  it.p_first = c * p.prow_chunk;
-  const int p_last = min(p.s.rank_k, (c + 1) * p.prow_chunk);
-  it.n_rk = max(0, p_last - it.p_first);
   const int tail_per = (n_tail + C - 1) / C;
   it.t_first = c * tail_per;
   it.n_tk = max(0, min(n_tail, it.t_first + tail_per) - it.t_first);
   it.c_first = c * p.chunk;
   it.chunk_len = max(0, min(p.s.n_comp, it.c_first + p.chunk) - it.c_first);
   it.tiles = (it.chunk_len + 127) / 128;
-  it.n_heads = 0;
-  for (int g = c; g < p.s.Hkv; g += C) ++it.n_heads;
-  it.nrb = (p.s.rank_v + 31) / 32;
-  it.rk0 = 0;
-  it.tk0 = it.n_rk;
-  it.lk0 = it.tk0 + it.n_tk;
-  const int after_lk = it.lk0 + it.tiles * p.kpk;
-  it.lv0 = after_lk + (after_lk & 1);  // pad to even: V panel pairs sit in adjacent stages
-  it.tv0 = it.lv0 + it.tiles * p.vpanels;
-  it.rv0 = it.tv0 + it.n_tk;
-  it.total = it.rv0 + it.n_heads * it.nrb;
+  // ring items (MMA operands only): left_k panels, even-pad, left_v panels
+  it.lk0 = 0;
+  const int after_lk = it.tiles * p.kpk;
+  it.lv0 = after_lk + (after_lk & 1);  // V panel pairs must sit in adjacent stages
+  it.total = it.lv0 + it.tiles * p.vpanels;
   return it;
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -147,10 +143,182 @@ __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bflo
   lo = __float2bfloat16_rn(x - __bfloat162float(hi));
 }
 
+// Streaming 16-byte global load that bypasses L1 (every byte is used once).
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void unpack8(const uint4& raw, float (&v)[8]) {
+  const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 f = __bfloat1622float2(h2[e]);
+    v[2 * e] = f.x;
+    v[2 * e + 1] = f.y;
+  }
+}
+
+// ============================================================================
+// 1. qdots: one block per (kv head g, instance b).  Rows = right_k (rank_k)
+//    then tail_k (n_tail); each lane owns 8 columns of the g-slice, D/8 lanes
+//    span one row segment and reduce with shuffles.
+// ============================================================================
+template <int PER_KV, int D>
+__global__ void __launch_bounds__(kStreamThreads) qdots_kernel(const FusedPlan p, const FusedArgs a) {
+  constexpr int LPH = D / 8, RPI = 32 / LPH;
+  const int g = blockIdx.x, b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = p.s.H, W = p.s.Hkv * D;
+  const int n_tail = a.n_tail_dev ? *a.n_tail_dev : a.n_tail;
+  const int rk = p.s.rank_k, rows = rk + n_tail;
+  const int col8 = (lane % LPH) * 8, rsub = lane / LPH;
+  const float scale = rsqrtf(static_cast<float>(D));
+  float qv[PER_KV][8];
+#pragma unroll
+  for (int y = 0; y < PER_KV; ++y)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) qv[y][e] = a.q[static_cast<long>(b) * H * D + (g * PER_KV + y) * D + col8 + e] * scale;
+  const __nv_bfloat16* rkb = a.right_k + static_cast<long>(b) * rk * W + g * D + col8;
+  const __nv_bfloat16* tkb = a.tail_k + static_cast<long>(b) * p.s.tail_cap * W + g * D + col8;
+  const int NP = p.np;
+  const uint32_t plane = static_cast<uint32_t>(p.kpk) * NP * 128;  // bytes of one (hi or lo) operand
+  unsigned char* pimg = a.ws_pimg + static_cast<size_t>(b) * 2 * plane;
+  float* tout = a.ws_tail + static_cast<long>(b) * H * p.s.tail_cap;
+  // zero padding of the operand image: ranks >= rank_k of my heads; heads >= H (block g == 0)
+  for (int i = threadIdx.x; i < PER_KV * (p.kpk * 64 - rk); i += kStreamThreads) {
+    const int h = g * PER_KV + i / (p.kpk * 64 - rk), r = rk + i % (p.kpk * 64 - rk);
+    const uint32_t off = (r >> 6) * NP * 128 + sw128_off(h, r & 63);
+    *reinterpret_cast<__nv_bfloat16*>(pimg + off) = __float2bfloat16_rn(0.f);
+    *reinterpret_cast<__nv_bfloat16*>(pimg + plane + off) = __float2bfloat16_rn(0.f);
+  }
+  if (g == 0)
+    for (int i = threadIdx.x; i < (NP - H) * p.kpk * 64; i += kStreamThreads) {
+      const int h = H + i / (p.kpk * 64), r = i % (p.kpk * 64);
+      const uint32_t off = (r >> 6) * NP * 128 + sw128_off(h, r & 63);
+      *reinterpret_cast<__nv_bfloat16*>(pimg + off) = __float2bfloat16_rn(0.f);
+      *reinterpret_cast<__nv_bfloat16*>(pimg + plane + off) = __float2bfloat16_rn(0.f);
+    }
+  constexpr int U = 8;
+  const int stride = 8 * RPI;  // rows advanced per warp-instruction round across the block
+  for (int r0 = warp * RPI + rsub; r0 < rows; r0 += U * stride) {
+    uint4 raw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = r0 + u * stride;
+      if (r < rows) raw[u] = ldg_stream(r < rk ? rkb + static_cast<long>(r) * W : tkb + static_cast<long>(r - rk) * W);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = r0 + u * stride;
+      float v[8];
+      unpack8(raw[u], v);
+#pragma unroll
+      for (int y = 0; y < PER_KV; ++y) {
+        float acc = v[0] * qv[y][0];
+#pragma unroll
+        for (int e = 1; e < 8; ++e) acc = fmaf(v[e], qv[y][e], acc);
+#pragma unroll
+        for (int o = LPH / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if ((lane % LPH) == 0 && r < rows) {
+          const int h = g * PER_KV + y;
+          if (r < rk) {
+            __nv_bfloat16 hi, lo;
+            split_bf16(acc, hi, lo);
+            const uint32_t off = (r >> 6) * NP * 128 + sw128_off(h, r & 63);
+            *reinterpret_cast<__nv_bfloat16*>(pimg + off) = hi;
+            *reinterpret_cast<__nv_bfloat16*>(pimg + plane + off) = lo;
+          } else {
+            tout[static_cast<long>(h) * p.s.tail_cap + (r - rk)] = acc;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ============================================================================
+// 3. vsum: out[h, :] = sum_r U[h, r] right_v[r, g-slice] + sum_t p_tail[h, t] tail_v[t, g-slice]
+// ============================================================================
+template <int PER_KV, int D>
+__global__ void __launch_bounds__(kStreamThreads) vsum_kernel(const FusedPlan p, const FusedArgs a) {
+  constexpr int LPH = D / 8, RPI = 32 / LPH, NPART = 8 * RPI;
+  extern __shared__ __align__(16) float vsm[];
+  const int g = blockIdx.x, b = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int H = p.s.H, W = p.s.Hkv * D;
+  const int n_tail = a.n_tail_dev ? *a.n_tail_dev : a.n_tail;
+  const int rv = p.s.rank_v, rows = rv + n_tail;
+  const int col8 = (lane % LPH) * 8, rsub = lane / LPH;
+  // weights for this block's query heads: [PER_KV][rows]
+  float* wts = vsm;
+  const int wstride = (rv + p.s.tail_cap + 3) & ~3;
+  float* red = vsm + PER_KV * wstride;
+  for (int i = threadIdx.x; i < PER_KV * rows; i += kStreamThreads) {
+    const int y = i / rows, r = i % rows, h = g * PER_KV + y;
+    wts[y * wstride + r] = r < rv ? a.ws_u[(static_cast<long>(b) * H + h) * rv + r]
+                                  : a.ws_tail[(static_cast<long>(b) * H + h) * p.s.tail_cap + (r - rv)];
+  }
+  __syncthreads();
+  const __nv_bfloat16* rvb = a.right_v + static_cast<long>(b) * rv * W + g * D + col8;
+  const __nv_bfloat16* tvb = a.tail_v + static_cast<long>(b) * p.s.tail_cap * W + g * D + col8;
+  float acc[PER_KV][8];
+#pragma unroll
+  for (int y = 0; y < PER_KV; ++y)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[y][e] = 0.f;
+  constexpr int U = 8;
+  const int stride = 8 * RPI;
+  for (int r0 = warp * RPI + rsub; r0 < rows; r0 += U * stride) {
+    uint4 raw[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = r0 + u * stride;
+      if (r < rows) raw[u] = ldg_stream(r < rv ? rvb + static_cast<long>(r) * W : tvb + static_cast<long>(r - rv) * W);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = r0 + u * stride;
+      if (r >= rows) break;
+      float v[8];
+      unpack8(raw[u], v);
+#pragma unroll
+      for (int y = 0; y < PER_KV; ++y) {
+        const float w = wts[y * wstride + r];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[y][e] = fmaf(w, v[e], acc[y][e]);
+      }
+    }
+  }
+  // reduce the NPART (warp, row-subset) partials of every column
+#pragma unroll
+  for (int y = 0; y < PER_KV; ++y) {
+    float* dst = red + ((warp * RPI + rsub) * PER_KV + y) * D + col8;
+    *reinterpret_cast<float4*>(dst) = make_float4(acc[y][0], acc[y][1], acc[y][2], acc[y][3]);
+    *reinterpret_cast<float4*>(dst + 4) = make_float4(acc[y][4], acc[y][5], acc[y][6], acc[y][7]);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < PER_KV * D; i += kStreamThreads) {
+    const int y = i / D, col = i % D;
+    float s = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < NPART; ++k) s += red[(k * PER_KV + y) * D + col];
+    const long oi = static_cast<long>(b) * H * D + static_cast<long>(g * PER_KV + y) * D + col;
+    if (a.ctx_bf16)
+      reinterpret_cast<__nv_bfloat16*>(a.ctx_out)[oi] = __float2bfloat16_rn(s);
+    else
+      reinterpret_cast<float*>(a.ctx_out)[oi] = s;
+  }
+}
+
+// ============================================================================
+// 2. core: one cluster of C CTAs per instance.
+// ============================================================================
 __global__ void __launch_bounds__(kThreads, 1)
-    fused_decode_kernel(const FusedPlan p, const __grid_constant__ CUtensorMap map_lk,
-                        const __grid_constant__ CUtensorMap map_lv, const __grid_constant__ CUtensorMap map_rv,
-                        const FusedArgs a) {
+    core_kernel(const FusedPlan p, const __grid_constant__ CUtensorMap map_lk,
+                const __grid_constant__ CUtensorMap map_lv, const FusedArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const Smem L = smem_layout(p);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -159,8 +327,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int C = p.s.cluster;
   const int c = static_cast<int>(cluster_rank());
   const int b = blockIdx.x / C;
-  const int H = p.s.H, Hkv = p.s.Hkv, D = p.s.D, W = Hkv * D, NP = p.np;
-  const int per_kv = H / Hkv;
+  const int H = p.s.H, NP = p.np;
   const int n_tail = a.n_tail_dev ? *a.n_tail_dev : a.n_tail;
   const Items it = make_items(p, c, n_tail);
   const uint32_t s_cols = static_cast<uint32_t>(p.max_tiles * NP);
@@ -168,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // ---- prologue: zero ring + P operand, barriers, TMEM -------------------------
   {
     uint4* z = reinterpret_cast<uint4*>(smem);
-    const uint32_t n16 = L.pt / 16;  // ring + P hi/lo
+    const uint32_t n16 = L.phi / 16;  // ring only (P arrives as a bulk copy)
     for (uint32_t i = threadIdx.x; i < n16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
   }
   if (threadIdx.x == 0) {
@@ -176,7 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&bars[kFull + s], 1);
       mbar_init(&bars[kEmpty + s], 1);
     }
-    for (int i = kPopReady; i <= kTmemFree; ++i) mbar_init(&bars[i], 1);
+    for (int i = kPopReady; i <= kTmemFree; ++i) mbar_init(&bars[i], 1);  // kPopReady: producer's expect_tx
     for (int i = kSlices; i <= kDone; ++i) mbar_init(&bars[i], C);
     fence_mbar_init();
   }
@@ -189,55 +356,40 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tslot;
 
   if (warp == 0) {
-    // ===================== producer =====================
+    // ===================== producer: left_k / left_v panels =====================
     if (lane == 0) {
       prefetch_tmap(&map_lk);
       prefetch_tmap(&map_lv);
-      prefetch_tmap(&map_rv);
-      const long wb = static_cast<long>(W) * 2;
+      {  // P operand image (bf16 hi/lo, already swizzled by qdots) -> smem in one bulk copy
+        const uint32_t pbytes = 2u * p.kpk * NP * 128;
+        mbar_expect_tx(&bars[kPopReady], pbytes);
+        bulk_load(smem + L.phi, reinterpret_cast<const unsigned char*>(a.ws_pimg) + static_cast<size_t>(b) * pbytes,
+                  pbytes, &bars[kPopReady]);
+      }
       for (int i = 0; i < it.total; ++i) {
         const int s = i % kStages;
         mbar_wait(&bars[kEmpty + s], ((i / kStages) & 1) ^ 1);
         unsigned char* dst = smem + L.ring + s * kStageBytes;
         uint64_t* full = &bars[kFull + s];
-        if (i < it.tk0) {  // right_k rows
-          const int r = it.p_first + (i - it.rk0);
-          mbar_expect_tx(full, static_cast<uint32_t>(wb));
-          bulk_load(dst, a.right_k + (static_cast<long>(b) * p.s.rank_k + r) * W, static_cast<uint32_t>(wb), full);
-        } else if (i < it.lk0) {  // tail_k rows
-          const int t = it.t_first + (i - it.tk0);
-          mbar_expect_tx(full, static_cast<uint32_t>(wb));
-          bulk_load(dst, a.tail_k + (static_cast<long>(b) * p.s.tail_cap + t) * W, static_cast<uint32_t>(wb), full);
-        } else if (i < it.lv0 || i < it.tv0) {  // left_k / left_v panels (or the even-pad slot)
-          const bool is_v = i >= it.lv0;
-          const int rel = is_v ? i - it.lv0 : i - it.lk0;
-          const int per_tile = is_v ? p.vpanels : p.kpk;
-          if (!is_v && rel >= it.tiles * p.kpk) {  // pad slot
-            mbar_arrive(full);
-            continue;
-          }
-          const int tile = rel / per_tile, panel = rel % per_tile;
-          const int rank = is_v ? p.s.rank_v : p.s.rank_k;
-          if (panel * 64 >= rank) {  // V pad panel: rows >= rank_v of U are never read
-            mbar_arrive(full);
-            continue;
-          }
-          const int row0 = tile * 128;
-          const int nbox = min(4, (it.chunk_len - row0 + 31) / 32);
-          mbar_expect_tx(full, static_cast<uint32_t>(nbox) * 4096u);
-          const int grow = b * p.s.n_comp + it.c_first + row0;
-          for (int k = 0; k < nbox; ++k)
-            tma_load_2d(dst + k * 4096, is_v ? &map_lv : &map_lk, panel * 64, grow + 32 * k, full);
-        } else if (i < it.rv0) {  // tail_v rows
-          const int t = it.t_first + (i - it.tv0);
-          mbar_expect_tx(full, static_cast<uint32_t>(wb));
-          bulk_load(dst, a.tail_v + (static_cast<long>(b) * p.s.tail_cap + t) * W, static_cast<uint32_t>(wb), full);
-        } else {  // right_v boxes [32 rows x D] for my kv heads
-          const int rel = i - it.rv0;
-          const int hg = c + (rel / it.nrb) * C, rb = rel % it.nrb;
-          mbar_expect_tx(full, static_cast<uint32_t>(D) * 64u);
-          tma_load_2d(dst, &map_rv, hg * D, b * p.s.rank_v + rb * 32, full);
+        const bool is_v = i >= it.lv0;
+        const int rel = is_v ? i - it.lv0 : i - it.lk0;
+        const int per_tile = is_v ? p.vpanels : p.kpk;
+        if (!is_v && rel >= it.tiles * p.kpk) {  // even-pad slot
+          mbar_arrive(full);
+          continue;
         }
+        const int tile = rel / per_tile, panel = rel % per_tile;
+        const int rank = is_v ? p.s.rank_v : p.s.rank_k;
+        if (panel * 64 >= rank) {  // V pad panel: U rows >= rank_v are never read
+          mbar_arrive(full);
+          continue;
+        }
+        const int row0 = tile * 128;
+        const int nbox = min(4, (it.chunk_len - row0 + 31) / 32);
+        mbar_expect_tx(full, static_cast<uint32_t>(nbox) * 4096u);
+        const int grow = b * p.s.n_comp + it.c_first + row0;
+        for (int k = 0; k < nbox; ++k)
+          tma_load_2d(dst + k * 4096, is_v ? &map_lv : &map_lk, panel * 64, grow + 32 * k, full);
       }
     }
   } else if (warp == 1) {
@@ -266,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_commit(&bars[kEmpty + s]);
         }
       }
-      if (it.lv0 > it.lk0 + it.tiles * p.kpk) {  // release the even-pad slot
+      if (it.lv0 > it.tiles * p.kpk) {  // release the even-pad slot
         const int i = it.lv0 - 1, s = i % kStages;
         mbar_wait(&bars[kFull + s], (i / kStages) & 1);
         mbar_arrive(&bars[kEmpty + s]);
@@ -307,176 +459,104 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== compute warps =====================
     const int cw = warp - 2;                 // 0..7
     const int tid = threadIdx.x - 64;        // 0..255
-    const float inv_sqrt_d = rsqrtf(static_cast<float>(D));
-    float* q = reinterpret_cast<float*>(smem + L.pt);  // alias: dead before p tiles are written
     float* stail = reinterpret_cast<float*>(smem + L.stail);
     float* part = reinterpret_cast<float*>(smem + L.part);
     float* stats = reinterpret_cast<float*>(smem + L.stats);
+    double* imps = reinterpret_cast<double*>(smem + L.imps);
     float* m_loc = stats;
     float* z_loc = stats + NP;
     float* m_g = stats + 2 * NP;
-    float* z_g = stats + 3 * NP;
-    const int dl = D / 32;  // columns per lane within one kv-head slice (D in {64, 128})
+    float* f_me = stats + 3 * NP;  // exp(m_loc - m_g) / z_g   (my tokens' softmax correction)
+    float* zi_g = stats + 4 * NP;  // 1 / z_g
+    float* scale_c = stats + 5 * NP;  // [C][NP]: exp(m_c - m_g) per peer
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 0] = global_ns();
 
-    for (int i = tid; i < H * D; i += kComputeThreads) q[i] = a.q[static_cast<long>(b) * H * D + i];
-    named_bar(kBarCompute, kComputeThreads);
-
-    // Per-row dot products against q: row = [W] bf16 in a ring stage.
-    // Writes out(h) for every query head h (lane 0 of the owning warp).
-    auto row_dots = [&](const __nv_bfloat16* row, auto&& emit) {
-      for (int g = cw; g < Hkv; g += 8) {
-        float v[4];
-        const __nv_bfloat16* src = row + g * D + lane * dl;
-        if (dl == 4) {
-          const uint2 raw = *reinterpret_cast<const uint2*>(src);
-          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-          const float2 f0 = __bfloat1622float2(h2[0]), f1 = __bfloat1622float2(h2[1]);
-          v[0] = f0.x; v[1] = f0.y; v[2] = f1.x; v[3] = f1.y;
-        } else {
-          const __nv_bfloat162 raw = *reinterpret_cast<const __nv_bfloat162*>(src);
-          const float2 f0 = __bfloat1622float2(raw);
-          v[0] = f0.x; v[1] = f0.y; v[2] = 0.f; v[3] = 0.f;
-        }
-        for (int hh = 0; hh < per_kv; ++hh) {
-          const int h = g * per_kv + hh;
-          const float* qh = q + h * D + lane * dl;
-          float acc = 0.f;
-          for (int e = 0; e < dl; ++e) acc = fmaf(v[e], qh[e], acc);
-          acc = warp_sum(acc);
-          if (lane == 0) emit(h, acc * inv_sqrt_d);
-        }
-      }
-    };
-    auto consume = [&](int i) {
-      mbar_wait(&bars[kFull + i % kStages], (i / kStages) & 1);
-      return reinterpret_cast<const __nv_bfloat16*>(smem + L.ring + (i % kStages) * kStageBytes);
-    };
-    auto release = [&](int i) {
-      named_bar(kBarCompute, kComputeThreads);
-      if (tid == 0) mbar_arrive(&bars[kEmpty + i % kStages]);
-    };
-
-    // ---- phase P: my slice of P = right_k q / sqrt(D), bf16 hi/lo, swizzled B operand
-    unsigned char* phi = smem + L.phi;
-    unsigned char* plo = smem + L.plo;
-    for (int j = 0; j < it.n_rk; ++j) {
-      const int i = it.rk0 + j, r = it.p_first + j;
-      const __nv_bfloat16* row = consume(i);
-      row_dots(row, [&](int h, float val) {
-        __nv_bfloat16 hi, lo;
-        split_bf16(val, hi, lo);
-        const uint32_t off = (r >> 6) * NP * 128 + sw128_off(h, r & 63);
-        *reinterpret_cast<__nv_bfloat16*>(phi + off) = hi;
-        *reinterpret_cast<__nv_bfloat16*>(plo + off) = lo;
-      });
-      release(i);
+    // prefetch my importance scores and tail logits (latency off the critical path)
+    const float* tg = a.ws_tail + static_cast<long>(b) * H * p.s.tail_cap;
+    if (a.importance) {
+      const double* ib = a.importance + static_cast<long>(b) * a.imp_stride;
+      for (int i = tid; i < it.chunk_len; i += kComputeThreads) imps[i] = ib[it.c_first + i];
+      for (int j = tid; j < it.n_tk; j += kComputeThreads) imps[p.chunk + j] = ib[p.s.n_comp + it.t_first + j];
     }
-    // ---- tail K scores
-    for (int j = 0; j < it.n_tk; ++j) {
-      const int i = it.tk0 + j;
-      const __nv_bfloat16* row = consume(i);
-      row_dots(row, [&](int h, float val) { stail[j * NP + h] = val; });
-      release(i);
+    for (int i = tid; i < it.n_tk * H; i += kComputeThreads) {
+      const int j = i % it.n_tk, h = i / it.n_tk;
+      stail[j * NP + h] = tg[static_cast<long>(h) * p.s.tail_cap + it.t_first + j];
     }
-    // ---- publish my P rows; assemble the full P operand from the peers
-    if (tid == 0) fence_acq_rel_cluster();
-    named_bar(kBarCompute, kComputeThreads);
-    if (tid < C) mbar_arrive_cluster(&bars[kSlices], static_cast<uint32_t>(tid));
-    mbar_wait_cluster(&bars[kSlices], 0);
-    for (int peer = 0; peer < C; ++peer) {
-      if (peer == c) continue;
-      const int r0 = peer * p.prow_chunk, r1 = min(p.s.rank_k, r0 + p.prow_chunk);
-      const int n_oct = max(0, (r1 - r0 + 7) / 8);
-      for (int w = tid; w < n_oct * NP * 2; w += kComputeThreads) {
-        const int which = w / (n_oct * NP), rem = w % (n_oct * NP);
-        const int oct = r0 / 8 + rem / NP, h = rem % NP;
-        const uint32_t off = (oct >> 3) * NP * 128 + sw128_off(h, (oct & 7) * 8);
-        unsigned char* base = which ? plo : phi;
-        *reinterpret_cast<uint4*>(base + off) = ld_dsmem_v4(base + off, static_cast<uint32_t>(peer));
-      }
-    }
-    fence_proxy_async();
-    named_bar(kBarCompute, kComputeThreads);
-    if (tid == 0) mbar_arrive(&bars[kPopReady]);
 
-    // ---- softmax statistics over my tokens, then cluster-wide
+    // ---- local softmax statistics (single online pass over TMEM-resident S + my tail logits)
     const int qd = warp & 3, hf = cw >> 2;  // TMEM lane quadrant, head half
     const int hcols = NP / 2, hbase = hf * hcols;
+    auto tmem_row = [&](uint32_t col) { return tmem + (static_cast<uint32_t>(qd * 32) << 16) + col; };
     mbar_wait(&bars[kSFull], 0);
     tc_fence_after();
-    auto tmem_row = [&](uint32_t col) { return tmem + (static_cast<uint32_t>(qd * 32) << 16) + col; };
-    for (int pass = 0; pass < 2; ++pass) {
-      // pass 0: max, pass 1: sum exp(s - m_loc)
-      for (int h0 = 0; h0 < hcols; h0 += 8) {
-        float acc[8];
-        for (int e = 0; e < 8; ++e) acc[e] = pass == 0 ? -INFINITY : 0.f;
-        for (int t = 0; t < it.tiles; ++t) {
-          float v[8];
-          tmem_ld8(tmem_row(static_cast<uint32_t>(t * NP + hbase + h0)), v);
-          const bool valid = t * 128 + qd * 32 + lane < it.chunk_len;
-          for (int e = 0; e < 8; ++e) {
-            const int h = hbase + h0 + e;
-            if (!valid || h >= H) continue;
-            acc[e] = pass == 0 ? fmaxf(acc[e], v[e]) : acc[e] + expf(v[e] - m_loc[h]);
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 1] = global_ns();
+    float* part_m = part;            // [8 warps][NP]
+    float* part_s = part + 8 * NP;   // [8 warps][NP]
+    for (int h0 = 0; h0 < hcols; h0 += 8) {
+      float mx[8], sm[8];
+      for (int e = 0; e < 8; ++e) {
+        mx[e] = -INFINITY;
+        sm[e] = 0.f;
+      }
+      for (int t = 0; t < it.tiles; ++t) {
+        float v[8];
+        tmem_ld8(tmem_row(static_cast<uint32_t>(t * NP + hbase + h0)), v);
+        if (t * 128 + qd * 32 + lane >= it.chunk_len) continue;
+        for (int e = 0; e < 8; ++e) {
+          if (v[e] > mx[e]) {
+            sm[e] = sm[e] * __expf(mx[e] - v[e]) + 1.f;
+            mx[e] = v[e];
+          } else {
+            sm[e] += __expf(v[e] - mx[e]);
           }
         }
-        for (int e = 0; e < 8; ++e) {
-          const float r = pass == 0 ? warp_max(acc[e]) : warp_sum(acc[e]);
-          if (lane == 0) part[(cw) * NP + hbase + h0 + e] = r;  // cw in [4hf, 4hf+3]: one per quadrant
+      }
+      for (int e = 0; e < 8; ++e) {
+        float m = mx[e], z = sm[e];
+        for (int o = 16; o > 0; o >>= 1) {
+          const float m2 = __shfl_xor_sync(0xffffffffu, m, o), z2 = __shfl_xor_sync(0xffffffffu, z, o);
+          const float mm = fmaxf(m, m2);
+          z = (mm == -INFINITY) ? 0.f : z * __expf(m - mm) + z2 * __expf(m2 - mm);
+          m = mm;
+        }
+        if (lane == 0) {
+          part_m[cw * NP + hbase + h0 + e] = m;
+          part_s[cw * NP + hbase + h0 + e] = z;
         }
       }
-      named_bar(kBarCompute, kComputeThreads);
-      if (tid < H) {
-        const int h = tid, hb = (h / hcols) * 4;
-        float r = pass == 0 ? -INFINITY : 0.f;
-        for (int w = 0; w < 4; ++w) r = pass == 0 ? fmaxf(r, part[(hb + w) * NP + h]) : r + part[(hb + w) * NP + h];
-        for (int j = 0; j < it.n_tk; ++j)
-          r = pass == 0 ? fmaxf(r, stail[j * NP + h]) : r + expf(stail[j * NP + h] - m_loc[h]);
-        if (pass == 0) m_loc[h] = r; else z_loc[h] = r;
-      }
-      named_bar(kBarCompute, kComputeThreads);
     }
-    if (tid == 0) fence_acq_rel_cluster();
     named_bar(kBarCompute, kComputeThreads);
-    if (tid < C) mbar_arrive_cluster(&bars[kStats], static_cast<uint32_t>(tid));
-    mbar_wait_cluster(&bars[kStats], 0);
     if (tid < H) {
-      const int h = tid;
-      float mg = -INFINITY;
-      for (int peer = 0; peer < C; ++peer) mg = fmaxf(mg, ld_dsmem_f32(&m_loc[h], static_cast<uint32_t>(peer)));
-      float zg = 0.f;
-      for (int peer = 0; peer < C; ++peer) {
-        const float mp = ld_dsmem_f32(&m_loc[h], static_cast<uint32_t>(peer));
-        const float zp = ld_dsmem_f32(&z_loc[h], static_cast<uint32_t>(peer));
-        if (zp > 0.f) zg += zp * expf(mp - mg);
+      const int h = tid, hb = (h / hcols) * 4;
+      float m = -INFINITY;
+      for (int w = 0; w < 4; ++w) m = fmaxf(m, part_m[(hb + w) * NP + h]);
+      for (int j = 0; j < it.n_tk; ++j) m = fmaxf(m, stail[j * NP + h]);
+      float z = 0.f;
+      for (int w = 0; w < 4; ++w) {
+        const float mw = part_m[(hb + w) * NP + h];
+        if (mw != -INFINITY) z += part_s[(hb + w) * NP + h] * __expf(mw - m);
       }
-      m_g[h] = mg;
-      z_g[h] = zg;
+      for (int j = 0; j < it.n_tk; ++j) z += __expf(stail[j * NP + h] - m);
+      m_loc[h] = m;
+      z_loc[h] = z;
     }
     named_bar(kBarCompute, kComputeThreads);
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 2] = global_ns();
 
-    // ---- p tiles (bf16 hi/lo B operand, K-major over tokens) + importance EMA
-    float* ha_half = part + 8 * NP;  // [2][128]
-    const float inv_h = 1.0f / static_cast<float>(H);
+    // ---- p tiles with the local max (bf16 hi/lo B operand, K-major over tokens)
     for (int t = 0; t < it.tiles; ++t) {
       const int buf = t & 1;
       if (t >= 2) mbar_wait(&bars[kPEmpty0 + buf], ((t - 2) >> 1) & 1);
       unsigned char* pth = smem + L.pt + buf * 4 * NP * 128;
       unsigned char* ptl = pth + 2 * NP * 128;
       const int row = qd * 32 + lane;  // token within the tile
-      const int tok = t * 128 + row;
-      const bool valid = tok < it.chunk_len;
-      float hsum = 0.f;
+      const bool valid = t * 128 + row < it.chunk_len;
       for (int h0 = 0; h0 < hcols; h0 += 8) {
         float v[8];
         tmem_ld8(tmem_row(static_cast<uint32_t>(t * NP + hbase + h0)), v);
         for (int e = 0; e < 8; ++e) {
           const int h = hbase + h0 + e;
-          float pv = 0.f;
-          if (valid && h < H) {
-            pv = expf(v[e] - m_g[h]);
-            hsum += pv / z_g[h];
-          }
+          const float pv = (valid && h < H) ? __expf(v[e] - m_loc[h]) : 0.f;
           __nv_bfloat16 hi, lo;
           split_bf16(pv, hi, lo);
           const uint32_t off = (row >> 6) * NP * 128 + sw128_off(h, row & 63);
@@ -484,75 +564,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<__nv_bfloat16*>(ptl + off) = lo;
         }
       }
-      ha_half[hf * 128 + row] = hsum;
       fence_proxy_async();
       named_bar(kBarCompute, kComputeThreads);
       if (tid == 0) mbar_arrive(&bars[kPFull0 + buf]);
-      if (tid < 128) {
-        const int tk = t * 128 + tid;
-        if (tk < it.chunk_len) {
-          const float ha = (ha_half[tid] + ha_half[128 + tid]) * inv_h;
-          const long gi = it.c_first + tk;
-          if (a.head_avg) a.head_avg[static_cast<long>(b) * (p.s.n_comp + p.s.tail_cap) + gi] = ha;
-          if (a.importance) {
-            double* imp = a.importance + static_cast<long>(b) * a.imp_stride + gi;
-            *imp = __dadd_rn(__dmul_rn(a.ema_decay, *imp), __dmul_rn(a.ema_blend, static_cast<double>(ha)));
-          }
-        }
-      }
-      named_bar(kBarCompute, kComputeThreads);
     }
-    // tail tokens: p in place of the scores, head average, EMA
+    // tail: local p in place of the logits
     for (int w = tid; w < it.n_tk * H; w += kComputeThreads) {
       const int j = w / H, h = w % H;
-      stail[j * NP + h] = expf(stail[j * NP + h] - m_g[h]);
+      stail[j * NP + h] = __expf(stail[j * NP + h] - m_loc[h]);
     }
-    named_bar(kBarCompute, kComputeThreads);
-    for (int j = tid; j < it.n_tk; j += kComputeThreads) {
-      float hs = 0.f;
-      for (int h = 0; h < H; ++h) hs += stail[j * NP + h] / z_g[h];
-      const float ha = hs * inv_h;
-      const long gi = p.s.n_comp + it.t_first + j;
-      if (a.head_avg) a.head_avg[static_cast<long>(b) * (p.s.n_comp + p.s.tail_cap) + gi] = ha;
-      if (a.importance) {
-        double* imp = a.importance + static_cast<long>(b) * a.imp_stride + gi;
-        *imp = __dadd_rn(__dmul_rn(a.ema_decay, *imp), __dmul_rn(a.ema_blend, static_cast<double>(ha)));
-      }
-    }
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 3] = global_ns();
 
-    // ---- tail V: c[h, :] += p[t, h] * tail_v[t, g-slice]  (registers until U completes)
-    float cacc[8][4];
-    for (int x = 0; x < 8; ++x)
-      for (int e = 0; e < 4; ++e) cacc[x][e] = 0.f;
-    for (int j = 0; j < it.n_tk; ++j) {
-      const int i = it.tv0 + j;
-      const __nv_bfloat16* row = consume(i);
-      int x = 0;
-      for (int g = cw; g < Hkv; g += 8) {
-        const __nv_bfloat16* src = row + g * D + lane * dl;
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (dl == 4) {
-          const uint2 raw = *reinterpret_cast<const uint2*>(src);
-          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-          const float2 f0 = __bfloat1622float2(h2[0]), f1 = __bfloat1622float2(h2[1]);
-          v[0] = f0.x; v[1] = f0.y; v[2] = f1.x; v[3] = f1.y;
-        } else {
-          const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(src));
-          v[0] = f0.x; v[1] = f0.y;
-        }
-        for (int hh = 0; hh < per_kv && x < 8; ++hh, ++x) {
-          const float pw = stail[j * NP + g * per_kv + hh];
-          for (int e = 0; e < 4; ++e) cacc[x][e] = fmaf(pw, v[e], cacc[x][e]);
-        }
-      }
-      release(i);
-    }
-
-    // ---- U readback (TMEM -> U_loc[h][r]) and tail-context publish
+    // ---- U readback (TMEM -> U_loc[h][r]); publish (m_loc, z_loc, U_loc) to the cluster
     mbar_wait(&bars[kUFull], 0);
     tc_fence_after();
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 4] = global_ns();
     float* uloc = reinterpret_cast<float*>(smem + L.uloc);
-    float* ctxloc = reinterpret_cast<float*>(smem + L.ctxloc);
     for (int mt = 0; mt < p.mtiles; ++mt) {
       const int r = mt * 128 + qd * 32 + lane;
       for (int h0 = 0; h0 < hcols; h0 += 8) {
@@ -564,106 +591,118 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    {
-      int x = 0;
-      for (int g = cw; g < Hkv; g += 8)
-        for (int hh = 0; hh < per_kv && x < 8; ++hh, ++x)
-          for (int e = 0; e < dl; ++e) ctxloc[(g * per_kv + hh) * D + lane * dl + e] = cacc[x][e];
-    }
-    tc_fence_before();
     if (tid == 0) fence_acq_rel_cluster();
     named_bar(kBarCompute, kComputeThreads);
-    if (tid == 0) mbar_arrive(&bars[kTmemFree]);
     if (tid < C) mbar_arrive_cluster(&bars[kUReady], static_cast<uint32_t>(tid));
     mbar_wait_cluster(&bars[kUReady], 0);
 
-    // ---- gather U rows / tail contexts of my output heads from the cluster
-    float* ufin = reinterpret_cast<float*>(smem + L.ufin);
-    float* tfin = reinterpret_cast<float*>(smem + L.tfin);
-    float* red = reinterpret_cast<float*>(smem + L.red);
-    const int my_q = it.n_heads * per_kv;
-    const int r4 = L.uloc_stride / 4;
-    for (int w = tid; w < my_q * r4; w += kComputeThreads) {
-      const int hl = w / r4, r = (w % r4) * 4;
-      const int h = (c + (hl / per_kv) * C) * per_kv + hl % per_kv;
-      float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int peer = 0; peer < C; ++peer) {
-        const uint4 u = ld_dsmem_v4(&uloc[h * L.uloc_stride + r], static_cast<uint32_t>(peer));
-        s4.x += __uint_as_float(u.x); s4.y += __uint_as_float(u.y);
-        s4.z += __uint_as_float(u.z); s4.w += __uint_as_float(u.w);
-      }
-      *reinterpret_cast<float4*>(&ufin[hl * L.uloc_stride + r]) = s4;
+    // ---- global softmax statistics from the peers' (m, z)
+    if (tid < H) {
+      const int h = tid;
+      float mp[8], zp[8];
+#pragma unroll
+      for (int peer = 0; peer < 8; ++peer)
+        if (peer < C) {
+          mp[peer] = ld_dsmem_f32(&m_loc[h], static_cast<uint32_t>(peer));
+          zp[peer] = ld_dsmem_f32(&z_loc[h], static_cast<uint32_t>(peer));
+        }
+      float mg = -INFINITY;
+#pragma unroll
+      for (int peer = 0; peer < 8; ++peer)
+        if (peer < C) mg = fmaxf(mg, mp[peer]);
+      float zg = 0.f;
+#pragma unroll
+      for (int peer = 0; peer < 8; ++peer)
+        if (peer < C) {
+          const float sc = mp[peer] == -INFINITY ? 0.f : __expf(mp[peer] - mg);
+          scale_c[peer * NP + h] = sc;
+          zg += zp[peer] * sc;
+        }
+      const float zi = 1.0f / zg;
+      m_g[h] = mg;
+      zi_g[h] = zi;
+      f_me[h] = (m_loc[h] == -INFINITY ? 0.f : __expf(m_loc[h] - mg)) * zi;
     }
-    for (int w = tid; w < my_q * (D / 4); w += kComputeThreads) {
-      const int hl = w / (D / 4), d = (w % (D / 4)) * 4;
-      const int h = (c + (hl / per_kv) * C) * per_kv + hl % per_kv;
+    named_bar(kBarCompute, kComputeThreads);
+
+    // ---- reduce-scatter U over the cluster: heads h = c, c + C, ...; U / z -> workspace
+    const int r4 = L.uloc_stride / 4;
+    const int my_heads = (H - c + C - 1) / C;
+    for (int w = tid; w < my_heads * r4; w += kComputeThreads) {
+      const int h = c + (w / r4) * C, r = (w % r4) * 4;
+      uint4 u[8];
+#pragma unroll
+      for (int peer = 0; peer < 8; ++peer)
+        if (peer < C) u[peer] = ld_dsmem_v4(&uloc[h * L.uloc_stride + r], static_cast<uint32_t>(peer));
       float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int peer = 0; peer < C; ++peer) {
-        const uint4 u = ld_dsmem_v4(&ctxloc[h * D + d], static_cast<uint32_t>(peer));
-        s4.x += __uint_as_float(u.x); s4.y += __uint_as_float(u.y);
-        s4.z += __uint_as_float(u.z); s4.w += __uint_as_float(u.w);
+#pragma unroll
+      for (int peer = 0; peer < 8; ++peer) {
+        if (peer >= C) break;
+        const float sc = scale_c[peer * NP + h];
+        s4.x = fmaf(sc, __uint_as_float(u[peer].x), s4.x);
+        s4.y = fmaf(sc, __uint_as_float(u[peer].y), s4.y);
+        s4.z = fmaf(sc, __uint_as_float(u[peer].z), s4.z);
+        s4.w = fmaf(sc, __uint_as_float(u[peer].w), s4.w);
       }
-      *reinterpret_cast<float4*>(&tfin[hl * D + d]) = s4;
+      const float zi = zi_g[h];
+      float* dst = a.ws_u + (static_cast<long>(b) * H + h) * p.s.rank_v + r;
+      const float vals[4] = {s4.x * zi, s4.y * zi, s4.z * zi, s4.w * zi};
+      for (int e = 0; e < 4; ++e)
+        if (r + e < p.s.rank_v) dst[e] = vals[e];
     }
     if (tid == 0) fence_acq_rel_cluster();
     named_bar(kBarCompute, kComputeThreads);
     if (tid < C) mbar_arrive_cluster(&bars[kDone], static_cast<uint32_t>(tid));
 
-    // ---- output: out[h, :] = (U[h,:] . right_v[:, g-slice] + c[h, :]) / z_h
-    // Thread owns 8 columns (16 B) of one row parity; warp cw covers rows 2cw, 2cw+1 (+16k).
-    const int col8 = (lane & 15) * 8, rpar = lane >> 4;
-    const int rows_per_box = 32;
-    for (int hl0 = 0; hl0 < it.n_heads; ++hl0) {
-      const int g = c + hl0 * C;
-      float oacc[4][8];
-      for (int x = 0; x < 4; ++x)
-        for (int e = 0; e < 8; ++e) oacc[x][e] = 0.f;
-      for (int rb = 0; rb < it.nrb; ++rb) {
-        const int i = it.rv0 + hl0 * it.nrb + rb;
-        const __nv_bfloat16* box = consume(i);
-        if (col8 < D) {
-          for (int k = 0; k < rows_per_box / 16; ++k) {
-            const int rr = 16 * k + 2 * cw + rpar;
-            const int r = rb * 32 + rr;
-            if (r < p.s.rank_v) {
-              const uint4 raw = *reinterpret_cast<const uint4*>(box + rr * D + col8);
-              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
-              float v[8];
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h2[e]);
-                v[2 * e] = f.x;
-                v[2 * e + 1] = f.y;
-              }
-              for (int hh = 0; hh < per_kv && hh < 4; ++hh) {
-                const float u = ufin[(hl0 * per_kv + hh) * L.uloc_stride + r];
-                for (int e = 0; e < 8; ++e) oacc[hh][e] = fmaf(u, v[e], oacc[hh][e]);
-              }
-            }
-          }
+    // ---- head-averaged attention + importance EMA (importance.cpp:33-65), S re-read from TMEM
+    float* ha_half = part;  // [2][128] (part_m / part_s are dead)
+    const float inv_h = 1.0f / static_cast<float>(H);
+    for (int t = 0; t < it.tiles; ++t) {
+      const int row = qd * 32 + lane;
+      float hsum = 0.f;
+      for (int h0 = 0; h0 < hcols; h0 += 8) {
+        float v[8];
+        tmem_ld8(tmem_row(static_cast<uint32_t>(t * NP + hbase + h0)), v);
+        for (int e = 0; e < 8; ++e) {
+          const int h = hbase + h0 + e;
+          if (h < H) hsum = fmaf(__expf(v[e] - m_loc[h]), f_me[h], hsum);
         }
-        release(i);
       }
-      // reduce the 16 (warp, row-parity) partials per column
-      if (col8 < D)
-        for (int hh = 0; hh < per_kv && hh < 4; ++hh)
-          for (int e = 0; e < 8; ++e) red[((cw * 2 + rpar) * per_kv + hh) * D + col8 + e] = oacc[hh][e];
+      ha_half[hf * 128 + row] = hsum;
       named_bar(kBarCompute, kComputeThreads);
-      for (int w = tid; w < per_kv * D; w += kComputeThreads) {
-        const int hh = w / D, col = w % D;
-        const int h = g * per_kv + hh;
-        float sacc = tfin[(hl0 * per_kv + hh) * D + col];
-        for (int k = 0; k < 16; ++k) sacc += red[(k * per_kv + hh) * D + col];
-        const float o = sacc / z_g[h];
-        const long oi = static_cast<long>(b) * H * D + static_cast<long>(h) * D + col;
-        if (a.ctx_bf16)
-          reinterpret_cast<__nv_bfloat16*>(a.ctx_out)[oi] = __float2bfloat16_rn(o);
-        else
-          reinterpret_cast<float*>(a.ctx_out)[oi] = o;
+      if (tid < 128) {
+        const int tk = t * 128 + tid;
+        if (tk < it.chunk_len) {
+          const float ha = (ha_half[tid] + ha_half[128 + tid]) * inv_h;
+          const long gi = it.c_first + tk;
+          if (a.head_avg) a.head_avg[static_cast<long>(b) * (p.s.n_comp + p.s.tail_cap) + gi] = ha;
+          if (a.importance)
+            a.importance[static_cast<long>(b) * a.imp_stride + gi] =
+                __dadd_rn(__dmul_rn(a.ema_decay, imps[tk]), __dmul_rn(a.ema_blend, static_cast<double>(ha)));
+        }
       }
       named_bar(kBarCompute, kComputeThreads);
     }
-    // peers may still be reading my U_loc / contexts
-    mbar_wait_cluster(&bars[kDone], 0);
+    tc_fence_before();
+    if (tid == 0) mbar_arrive(&bars[kTmemFree]);
+    // tail tokens: normalised p -> workspace (for vsum), head average, EMA
+    for (int w = tid; w < it.n_tk * H; w += kComputeThreads) {
+      const int j = w % it.n_tk, h = w / it.n_tk;
+      const float pn = stail[j * NP + h] * f_me[h];
+      a.ws_tail[(static_cast<long>(b) * H + h) * p.s.tail_cap + it.t_first + j] = pn;
+    }
+    for (int j = tid; j < it.n_tk; j += kComputeThreads) {
+      float hs = 0.f;
+      for (int h = 0; h < H; ++h) hs = fmaf(stail[j * NP + h], f_me[h], hs);
+      const float ha = hs * inv_h;
+      const long gi = p.s.n_comp + it.t_first + j;
+      if (a.head_avg) a.head_avg[static_cast<long>(b) * (p.s.n_comp + p.s.tail_cap) + gi] = ha;
+      if (a.importance)
+        a.importance[static_cast<long>(b) * a.imp_stride + gi] =
+            __dadd_rn(__dmul_rn(a.ema_decay, imps[p.chunk + j]), __dmul_rn(a.ema_blend, static_cast<double>(ha)));
+    }
+    mbar_wait_cluster(&bars[kDone], 0);  // peers may still be reading my U_loc / stats
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 5] = global_ns();
   }
 }
 
@@ -702,13 +741,13 @@ FusedPlan plan_fused(const FusedShape& s) {
     return p;
   };
   if (s.H % s.Hkv != 0) return bad("num_kv_heads must divide num_query_heads");
+  const int per_kv = s.H / s.Hkv;
+  if (per_kv != 1 && per_kv != 2 && per_kv != 4) return bad("fused path needs 1, 2 or 4 query heads per kv head");
   if (s.D != 128 && s.D != 64) return bad("fused path needs head_dim 64 or 128");
   if (s.H > 128) return bad("fused path supports up to 128 query heads");
-  if (s.H / s.Hkv > 4) return bad("fused path supports up to 4 query heads per kv head");
-  const int W = s.Hkv * s.D;
-  if (W * 2 > static_cast<int>(kStageBytes)) return bad("cache width exceeds one ring stage");
   if (s.rank_k < 1 || s.rank_v < 1) return bad("fused path needs low-rank K and V");
-  if (s.ld_left % 8 != 0 || s.ld_left < std::max(s.rank_k, s.rank_v)) return bad("left-factor stride must be a multiple of 8");
+  if (s.ld_left % 8 != 0 || s.ld_left < std::max(s.rank_k, s.rank_v))
+    return bad("left-factor stride must be a multiple of 8 and cover both ranks");
   if (s.cluster < 1 || s.cluster > 8) return bad("cluster size must be 1..8");
   p.np = (s.H + 15) / 16 * 16;
   p.kpk = (s.rank_k + 63) / 64;
@@ -719,39 +758,72 @@ FusedPlan plan_fused(const FusedShape& s) {
   p.max_tiles = (p.chunk + 127) / 128;
   p.tail_max = (s.tail_cap + s.cluster - 1) / s.cluster;
   if (p.tail_max > kTailMax) return bad("too many tail tokens per CTA (raise the cluster size)");
-  const int prow = (s.rank_k + s.cluster - 1) / s.cluster;
-  p.prow_chunk = (prow + 7) / 8 * 8;
-  p.heads_per_cta = (s.Hkv + s.cluster - 1) / s.cluster;
+  p.heads_per_cta = (s.H + s.cluster - 1) / s.cluster;
   const int cols = p.max_tiles * p.np + p.mtiles * p.np;
   if (cols > 512) return bad("TMEM budget exceeded (raise the cluster size)");
   p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   const Smem L = smem_layout(p);
-  const uint32_t late = L.red + 16 * (s.H / s.Hkv) * s.D * 4;
-  if (late > L.stail) return bad("late-phase buffers do not fit the operand region");
   p.smem_bytes = L.total;
   if (p.smem_bytes > 227 * 1024) return bad("shared-memory budget exceeded");
+  const size_t vs = (static_cast<size_t>(per_kv) * ((s.rank_v + s.tail_cap + 3) & ~3) + 8 * (256 / s.D) * per_kv * s.D) * 4;
+  if (vs > 200 * 1024) return bad("vsum weights exceed shared memory");
   p.ok = true;
   p.why = "";
   return p;
 }
 
-void encode_fused_maps(const FusedShape& s, const void* left_k, const void* left_v, const void* right_v,
-                       CUtensorMap* maps) {
+size_t fused_workspace_bytes(const FusedShape& s) {
+  const size_t np = (s.H + 15) / 16 * 16, kpk = (s.rank_k + 63) / 64;
+  const size_t pimg = 2 * kpk * np * 128;
+  return static_cast<size_t>(s.batch) * (pimg + sizeof(float) * s.H * (static_cast<size_t>(s.tail_cap) + s.rank_v));
+}
+
+void encode_fused_maps(const FusedShape& s, const void* left_k, const void* left_v, CUtensorMap* maps) {
   const uint64_t rows = static_cast<uint64_t>(s.batch) * s.n_comp;
   encode_2d(&maps[0], left_k, s.rank_k, rows, static_cast<uint64_t>(s.ld_left) * 2, 64, 32,
             CU_TENSOR_MAP_SWIZZLE_128B);
   encode_2d(&maps[1], left_v, s.rank_v, rows, static_cast<uint64_t>(s.ld_left) * 2, 64, 32,
             CU_TENSOR_MAP_SWIZZLE_128B);
-  const uint64_t W = static_cast<uint64_t>(s.Hkv) * s.D;
-  encode_2d(&maps[2], right_v, W, static_cast<uint64_t>(s.batch) * s.rank_v, W * 2, s.D, 32,
-            CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+template <int PER_KV, int D>
+void launch_stream_pair(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, bool first) {
+  const dim3 grid(static_cast<unsigned>(p.s.Hkv), static_cast<unsigned>(p.s.batch));
+  if (first) {
+    qdots_kernel<PER_KV, D><<<grid, kStreamThreads, 0, st>>>(p, a);
+    KVP_LAUNCHED();
+  } else {
+    const size_t smem = (static_cast<size_t>(PER_KV) * ((p.s.rank_v + p.s.tail_cap + 3) & ~3) + 8 * (256 / D) * PER_KV * D) * 4;
+    static size_t attr = 0;
+    if (attr < smem) {
+      KVP_CUDA(cudaFuncSetAttribute(vsum_kernel<PER_KV, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem)));
+      attr = smem;
+    }
+    vsum_kernel<PER_KV, D><<<grid, kStreamThreads, smem, st>>>(p, a);
+    KVP_LAUNCHED();
+  }
+}
+
+void launch_stream(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, bool first) {
+  const int per_kv = p.s.H / p.s.Hkv;
+  if (p.s.D == 128) {
+    if (per_kv == 1) launch_stream_pair<1, 128>(p, a, st, first);
+    else if (per_kv == 2) launch_stream_pair<2, 128>(p, a, st, first);
+    else launch_stream_pair<4, 128>(p, a, st, first);
+  } else {
+    if (per_kv == 1) launch_stream_pair<1, 64>(p, a, st, first);
+    else if (per_kv == 2) launch_stream_pair<2, 64>(p, a, st, first);
+    else launch_stream_pair<4, 64>(p, a, st, first);
+  }
 }
 
 void launch_fused(const FusedPlan& p, const CUtensorMap* maps, const FusedArgs& a, cudaStream_t st) {
   require(p.ok, KVP_ERR_PARAMETER, p.why);
+  launch_stream(p, a, st, true);
   static size_t attr_bytes = 0;
   if (attr_bytes < p.smem_bytes) {
-    KVP_CUDA(cudaFuncSetAttribute(fused_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    KVP_CUDA(cudaFuncSetAttribute(core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(p.smem_bytes)));
     attr_bytes = p.smem_bytes;
   }
@@ -767,11 +839,75 @@ void launch_fused(const FusedPlan& p, const CUtensorMap* maps, const FusedArgs& 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  KVP_CUDA(cudaLaunchKernelEx(&cfg, fused_decode_kernel, p, maps[0], maps[1], maps[2], a));
+  KVP_CUDA(cudaLaunchKernelEx(&cfg, core_kernel, p, maps[0], maps[1], a));
   KVP_LAUNCHED();
+  launch_stream(p, a, st, false);
+}
+
+int max_active_clusters(const FusedPlan& p) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(p.s.batch * p.s.cluster));
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = p.smem_bytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = static_cast<unsigned>(p.s.cluster);
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KVP_CUDA(cudaFuncSetAttribute(core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(p.smem_bytes)));
+  int n = 0;
+  KVP_CUDA(cudaOccupancyMaxActiveClusters(&n, core_kernel, &cfg));
+  return n;
 }
 
 }  // namespace kvp
+
+// Debug hooks (not part of the public header).
+static unsigned long long* g_trace = nullptr;
+extern "C" void kvp_debug_fused_trace(void* dev_buffer) { g_trace = static_cast<unsigned long long*>(dev_buffer); }
+
+namespace {
+// Cluster size: the largest of {8, 4, 2, 1} whose plan fits and that keeps
+// the whole batch in the fewest waves of co-resident clusters.
+int auto_cluster(kvp::FusedShape s) {
+  static std::map<std::tuple<int, int, int, int, int, int, int, int>, int> cache;
+  const auto key = std::make_tuple(s.H, s.Hkv, s.D, s.n_comp, s.rank_k, s.rank_v, s.tail_cap, s.batch);
+  if (auto it = cache.find(key); it != cache.end()) return it->second;
+  int best = 8, best_waves = 1 << 30;
+  for (int c : {8, 4, 2, 1}) {
+    s.cluster = c;
+    const kvp::FusedPlan p = kvp::plan_fused(s);
+    if (!p.ok) continue;
+    const int active = std::max(1, kvp::max_active_clusters(p));
+    const int waves = (s.batch + active - 1) / active;
+    if (waves < best_waves) {
+      best_waves = waves;
+      best = c;
+    }
+  }
+  cache[key] = best;
+  return best;
+}
+kvp::FusedShape shape_of(const kvp_fused_desc* d) {
+  kvp::FusedShape s{d->heads, d->kv_heads, d->head_dim, d->n_comp, d->rank_k, d->rank_v, d->ld_left,
+                    d->tail_cap, d->batch, d->cluster};
+  if (s.cluster <= 0) s.cluster = auto_cluster(s);
+  return s;
+}
+}  // namespace
+
+extern "C" int kvp_debug_fused_max_clusters(const kvp_fused_desc* d) {
+  int n = -1;
+  kvp::guarded([&] { n = kvp::max_active_clusters(kvp::plan_fused(shape_of(d))); });
+  return n;
+}
+
+extern "C" size_t kvp_decode_fused_workspace(const kvp_fused_desc* d) {
+  return d ? kvp::fused_workspace_bytes(shape_of(d)) : 0;
+}
 
 extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
   return kvp::guarded([&] {
@@ -783,12 +919,21 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     require(d->n_tail_dev != nullptr || (d->n_tail >= 0 && d->n_tail <= d->tail_cap), KVP_ERR_SHAPE,
             "decode_fused: tail length exceeds capacity");
     require(d->alpha >= 0.0 && d->alpha <= 1.0, KVP_ERR_PARAMETER, "update_importance: alpha must be in [0, 1]");
-    FusedShape s{d->heads, d->kv_heads, d->head_dim, d->n_comp, d->rank_k, d->rank_v, d->ld_left,
-                 d->tail_cap, d->batch, d->cluster > 0 ? d->cluster : 8};
+    const FusedShape s = shape_of(d);
     const FusedPlan p = plan_fused(s);
     require(p.ok, KVP_ERR_PARAMETER, (std::string("decode_fused: ") + p.why).c_str());
-    CUtensorMap maps[3];
-    encode_fused_maps(s, d->left_k, d->left_v, d->right_v, maps);
+    const size_t ws_bytes = fused_workspace_bytes(s);
+    cudaStream_t st = as_stream(stream);
+    std::unique_ptr<Scratch> own;
+    float* ws = static_cast<float*>(d->workspace);
+    if (ws == nullptr) {
+      own = std::make_unique<Scratch>(ws_bytes, st);
+      ws = own->as<float>();
+    } else {
+      require(d->workspace_bytes >= ws_bytes, KVP_ERR_PARAMETER, "decode_fused: workspace too small");
+    }
+    CUtensorMap maps[2];
+    encode_fused_maps(s, d->left_k, d->left_v, maps);
     FusedArgs a{};
     a.right_k = static_cast<const __nv_bfloat16*>(d->right_k);
     a.right_v = static_cast<const __nv_bfloat16*>(d->right_v);
@@ -797,7 +942,6 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     a.n_tail_dev = d->n_tail_dev;
     a.n_tail = d->n_tail;
     a.q = d->queries;
-    a.rank_v_tok = nullptr;
     a.importance = d->importance;
     a.imp_stride = d->imp_stride;
     const double decay = std::pow(d->alpha, 1.0);  // alpha^T_q, importance.cpp:58
@@ -806,6 +950,10 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     a.head_avg = d->head_avg;
     a.ctx_out = d->context;
     a.ctx_bf16 = d->context_bf16;
-    launch_fused(p, maps, a, as_stream(stream));
+    a.ws_pimg = reinterpret_cast<unsigned char*>(ws);
+    a.ws_tail = reinterpret_cast<float*>(a.ws_pimg + static_cast<size_t>(s.batch) * 2 * p.kpk * p.np * 128);
+    a.ws_u = a.ws_tail + static_cast<size_t>(s.batch) * s.H * s.tail_cap;
+    a.trace = g_trace;
+    launch_fused(p, maps, a, st);
   });
 }

@@ -1,10 +1,12 @@
-// Fused compressed-cache decode attention (bf16 storage, T_q = 1) — the
-// serving hot path.  See decode_fused.cu for the algorithm.
+// Compressed-cache decode attention (bf16 storage, T_q = 1), the serving hot
+// path: three launches per layer, see decode_fused.cu.
 #pragma once
 
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 
 namespace kvp {
@@ -16,26 +18,29 @@ struct FusedShape {
   int ld_left;        // row stride of left factors (elements, multiple of 8)
   int tail_cap;       // tail rows allocated per instance
   int batch;
-  int cluster;        // CTAs per instance
+  int cluster;        // CTAs per instance in the low-rank core kernel
 };
 
 struct FusedArgs {
-  // left factors are addressed through tensor maps (rows = batch*n_comp);
-  // right factors / tails through raw pointers.
   const __nv_bfloat16* right_k;  // [batch][rank_k][W]
-  const __nv_bfloat16* right_v;  // [batch][rank_v][W]  (also via tmap_rv)
+  const __nv_bfloat16* right_v;  // [batch][rank_v][W]
   const __nv_bfloat16* tail_k;   // [batch][tail_cap][W]
   const __nv_bfloat16* tail_v;
   const int* n_tail_dev;         // device counter of valid tail rows (nullable)
   int n_tail;                    // used when n_tail_dev == nullptr
   const float* q;                // [batch][H*D], raw (unscaled) queries
-  const uint16_t* rank_v_tok;    // [batch][n_comp] value rank prefix per token (nullable = full)
   double* importance;            // [batch][imp_stride]: compressed then tail (nullable)
   long imp_stride;
   double ema_decay, ema_blend;   // alpha^1, 1 - alpha^1 (T_q = 1)
   float* head_avg;               // [batch][n_comp + tail_cap] (nullable)
   void* ctx_out;                 // [batch][H*D]
   int ctx_bf16;                  // 1: bf16 output, 0: fp32
+  // workspace: P operand image (bf16 hi/lo, swizzled) [batch][2][kpk][NP][64],
+  //            s_tail / p_tail fp32 [batch][H][tail_cap], U fp32 [batch][H][rank_v]
+  unsigned char* ws_pimg;
+  float* ws_tail;
+  float* ws_u;
+  unsigned long long* trace;     // debug: per-CTA phase timestamps [grid][16] (nullable)
 };
 
 struct FusedPlan {
@@ -47,8 +52,7 @@ struct FusedPlan {
   int chunk;           // compressed tokens per CTA (multiple of 32)
   int max_tiles;       // ceil(chunk / 128)
   int tail_max;        // max tail tokens per CTA
-  int prow_chunk;      // P rows per CTA (multiple of 8)
-  int heads_per_cta;   // kv heads per CTA in the output phase (ceil)
+  int heads_per_cta;   // query heads per CTA in the U reduce-scatter
   size_t smem_bytes;
   int tmem_cols;
   bool ok;
@@ -56,11 +60,8 @@ struct FusedPlan {
 };
 
 FusedPlan plan_fused(const FusedShape& s);
-
-// Encodes the three tensor maps (left_k, left_v, right_v) for `base` pointers.
-void encode_fused_maps(const FusedShape& s, const void* left_k, const void* left_v, const void* right_v,
-                       CUtensorMap* maps /*[3]*/);
-
+size_t fused_workspace_bytes(const FusedShape& s);
+void encode_fused_maps(const FusedShape& s, const void* left_k, const void* left_v, CUtensorMap* maps /*[2]*/);
 void launch_fused(const FusedPlan& p, const CUtensorMap* maps, const FusedArgs& a, cudaStream_t st);
 
 }  // namespace kvp

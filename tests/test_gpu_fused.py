@@ -27,7 +27,8 @@ class FusedDesc(C.Structure):
                 ("left_k", C.c_void_p), ("right_k", C.c_void_p), ("left_v", C.c_void_p), ("right_v", C.c_void_p),
                 ("tail_k", C.c_void_p), ("tail_v", C.c_void_p), ("queries", C.c_void_p),
                 ("importance", C.c_void_p), ("imp_stride", C.c_int64), ("alpha", C.c_double),
-                ("head_avg", C.c_void_p), ("context", C.c_void_p)]
+                ("head_avg", C.c_void_p), ("context", C.c_void_p), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t)]
 
 
 def bf16_round(x):
