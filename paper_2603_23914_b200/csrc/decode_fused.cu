@@ -32,6 +32,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <memory>
 #include <tuple>
@@ -46,10 +47,11 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kStages = 6;  // even: V panel pairs never straddle the ring wrap
+constexpr int kMaxStages = 12;  // ring stages (even: V panel pairs never straddle the ring wrap)
 constexpr uint32_t kStageBytes = 16384;
-constexpr int kThreads = 320;
-constexpr int kComputeThreads = 256;
+constexpr int kThreads = 576;         // warp 0 TMA, warp 1 MMA, warps 2..17 compute
+constexpr int kComputeThreads = 512;
+constexpr int kComputeWarps = 16;
 constexpr uint32_t kBarCompute = 1;  // named barrier id for the compute warps
 constexpr int kTailMax = 96;
 constexpr int kStreamThreads = 256;  // qdots / vsum blocks
@@ -66,7 +68,7 @@ __host__ __device__ inline Smem smem_layout(const FusedPlan& p) {
   Smem s{};
   const uint32_t np = p.np;
   s.ring = 0;
-  s.phi = s.ring + kStages * kStageBytes;
+  s.phi = s.ring + p.stages * kStageBytes;
   s.plo = s.phi + p.kpk * np * 128;
   s.pt = align_up(s.plo + p.kpk * np * 128, 1024);  // 2 buffers x {hi, lo} x 2 panels
   const uint32_t pt_end = s.pt + 8 * np * 128;
@@ -75,18 +77,18 @@ __host__ __device__ inline Smem smem_layout(const FusedPlan& p) {
   const uint32_t uloc_end = s.uloc + np * s.uloc_stride * 4;
   s.stail = align_up(pt_end > uloc_end ? pt_end : uloc_end, 16);
   s.part = s.stail + p.tail_max * np * 4;
-  s.stats = s.part + 16 * np * 4 + 2 * 128 * 4;
+  s.stats = s.part + 2 * kComputeWarps * np * 4 + 4 * 128 * 4;
   s.imps = align_up(s.stats + (5 + 8) * np * 4, 16);
   s.bars = align_up(s.imps + (p.chunk + p.tail_max) * 8, 8);
-  s.tslot = s.bars + 32 * 8;
+  s.tslot = s.bars + 40 * 8;
   s.total = align_up(s.tslot + 16, 1024);
   return s;
 }
 
 enum Bar : int {
-  kFull = 0,                      // [kStages]
-  kEmpty = kStages,               // [kStages]
-  kPopReady = 2 * kStages,        // P operand assembled (compute -> MMA)
+  kFull = 0,                      // [kMaxStages]
+  kEmpty = kMaxStages,            // [kMaxStages]
+  kPopReady = 2 * kMaxStages,     // P operand image landed (producer bulk copy -> MMA)
   kSFull,                         // S MMAs complete (MMA -> compute)
   kPFull0, kPFull1,               // p tile buffer ready (compute -> MMA)
   kPEmpty0, kPEmpty1,             // p tile buffer consumed (MMA -> compute)
@@ -316,9 +318,11 @@ __global__ void __launch_bounds__(kStreamThreads) vsum_kernel(const FusedPlan p,
 // ============================================================================
 // 2. core: one cluster of C CTAs per instance.
 // ============================================================================
+template <int NPT>
 __global__ void __launch_bounds__(kThreads, 1)
     core_kernel(const FusedPlan p, const __grid_constant__ CUtensorMap map_lk,
-                const __grid_constant__ CUtensorMap map_lv, const FusedArgs a) {
+                const __grid_constant__ CUtensorMap map_lv, const __grid_constant__ CUtensorMap map_lk32,
+                const __grid_constant__ CUtensorMap map_lv32, const FusedArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const Smem L = smem_layout(p);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -327,10 +331,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int C = p.s.cluster;
   const int c = static_cast<int>(cluster_rank());
   const int b = blockIdx.x / C;
-  const int H = p.s.H, NP = p.np;
+  const int H = p.s.H;
+  constexpr int NP = NPT;
   const int n_tail = a.n_tail_dev ? *a.n_tail_dev : a.n_tail;
   const Items it = make_items(p, c, n_tail);
   const uint32_t s_cols = static_cast<uint32_t>(p.max_tiles * NP);
+  const int NS = p.stages;
 
   // ---- prologue: zero ring + P operand, barriers, TMEM -------------------------
   {
@@ -339,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (uint32_t i = threadIdx.x; i < n16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
   }
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
+    for (int s = 0; s < p.stages; ++s) {
       mbar_init(&bars[kFull + s], 1);
       mbar_init(&bars[kEmpty + s], 1);
     }
@@ -360,6 +366,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       prefetch_tmap(&map_lk);
       prefetch_tmap(&map_lv);
+      prefetch_tmap(&map_lk32);
+      prefetch_tmap(&map_lv32);
       {  // P operand image (bf16 hi/lo, already swizzled by qdots) -> smem in one bulk copy
         const uint32_t pbytes = 2u * p.kpk * NP * 128;
         mbar_expect_tx(&bars[kPopReady], pbytes);
@@ -367,8 +375,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                   pbytes, &bars[kPopReady]);
       }
       for (int i = 0; i < it.total; ++i) {
-        const int s = i % kStages;
-        mbar_wait(&bars[kEmpty + s], ((i / kStages) & 1) ^ 1);
+        const int s = i % NS;
+        mbar_wait(&bars[kEmpty + s], ((i / NS) & 1) ^ 1);
         unsigned char* dst = smem + L.ring + s * kStageBytes;
         uint64_t* full = &bars[kFull + s];
         const bool is_v = i >= it.lv0;
@@ -384,12 +392,17 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_arrive(full);
           continue;
         }
+        if (a.trace && i == it.lv0) a.trace[blockIdx.x * 16ull + 10] = global_ns();
         const int row0 = tile * 128;
         const int nbox = min(4, (it.chunk_len - row0 + 31) / 32);
         mbar_expect_tx(full, static_cast<uint32_t>(nbox) * 4096u);
         const int grow = b * p.s.n_comp + it.c_first + row0;
-        for (int k = 0; k < nbox; ++k)
-          tma_load_2d(dst + k * 4096, is_v ? &map_lv : &map_lk, panel * 64, grow + 32 * k, full);
+        if (nbox == 4 && !p.box32_only) {  // full 128-token tile: one 16 KB box
+          tma_load_2d(dst, is_v ? &map_lv : &map_lk, panel * 64, grow, full);
+        } else {
+          for (int k = 0; k < nbox; ++k)
+            tma_load_2d(dst + k * 4096, is_v ? &map_lv32 : &map_lk32, panel * 64, grow + 32 * k, full);
+        }
       }
     }
   } else if (warp == 1) {
@@ -402,10 +415,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t pt = smem_addr(smem + L.pt);
       mbar_wait(&bars[kPopReady], 0);
       tc_fence_after();
+      if (a.trace) a.trace[blockIdx.x * 16ull + 8] = global_ns();
       for (int t = 0; t < it.tiles; ++t) {
         for (int kp = 0; kp < p.kpk; ++kp) {
-          const int i = it.lk0 + t * p.kpk + kp, s = i % kStages;
-          mbar_wait(&bars[kFull + s], (i / kStages) & 1);
+          const int i = it.lk0 + t * p.kpk + kp, s = i % NS;
+          mbar_wait(&bars[kFull + s], (i / NS) & 1);
           tc_fence_after();
           for (int kk = 0; kk < 4; ++kk) {
             const uint64_t ad = smem_desc(ring + s * kStageBytes + kk * 32, 16, 1024, kSwizzle128B);
@@ -419,11 +433,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       if (it.lv0 > it.tiles * p.kpk) {  // release the even-pad slot
-        const int i = it.lv0 - 1, s = i % kStages;
-        mbar_wait(&bars[kFull + s], (i / kStages) & 1);
+        const int i = it.lv0 - 1, s = i % NS;
+        mbar_wait(&bars[kFull + s], (i / NS) & 1);
         mbar_arrive(&bars[kEmpty + s]);
       }
       mma_commit(&bars[kSFull]);
+      if (a.trace) a.trace[blockIdx.x * 16ull + 9] = global_ns();
       for (int t = 0; t < it.tiles; ++t) {
         const int buf = t & 1;
         mbar_wait(&bars[kPFull0 + buf], (t >> 1) & 1);
@@ -431,9 +446,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t pth = pt + buf * 4 * NP * 128, ptl = pth + 2 * NP * 128;
         for (int mt = 0; mt < p.mtiles; ++mt) {
           const int i0 = it.lv0 + t * p.vpanels + 2 * mt;
-          const int s0 = i0 % kStages, s1 = (i0 + 1) % kStages;
-          mbar_wait(&bars[kFull + s0], (i0 / kStages) & 1);
-          mbar_wait(&bars[kFull + s1], ((i0 + 1) / kStages) & 1);
+          const int s0 = i0 % NS, s1 = (i0 + 1) % NS;
+          mbar_wait(&bars[kFull + s0], (i0 / NS) & 1);
+          mbar_wait(&bars[kFull + s1], ((i0 + 1) / NS) & 1);
           tc_fence_after();
           const uint32_t d = tmem + s_cols + static_cast<uint32_t>(mt * NP);
           for (int ks = 0; ks < 8; ++ks) {
@@ -457,8 +472,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tmem_dealloc(tmem, static_cast<uint32_t>(p.tmem_cols));
   } else {
     // ===================== compute warps =====================
-    const int cw = warp - 2;                 // 0..7
-    const int tid = threadIdx.x - 64;        // 0..255
+    const int cw = warp - 2;                 // 0..15
+    const int tid = threadIdx.x - 64;        // 0..511
     float* stail = reinterpret_cast<float*>(smem + L.stail);
     float* part = reinterpret_cast<float*>(smem + L.part);
     float* stats = reinterpret_cast<float*>(smem + L.stats);
@@ -483,67 +498,46 @@ __global__ void __launch_bounds__(kThreads, 1)
       stail[j * NP + h] = tg[static_cast<long>(h) * p.s.tail_cap + it.t_first + j];
     }
 
-    // ---- local softmax statistics (single online pass over TMEM-resident S + my tail logits)
-    const int qd = warp & 3, hf = cw >> 2;  // TMEM lane quadrant, head half
-    const int hcols = NP / 2, hbase = hf * hcols;
+    // ---- local softmax: max over TMEM-resident S + my tail logits (no exponentials)
+    const int qd = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int cg = cw >> 2;                  // column group 0..3
+    constexpr int gcols = NP / 4;            // multiple of 4 columns
+    const int gbase = cg * gcols;
     auto tmem_row = [&](uint32_t col) { return tmem + (static_cast<uint32_t>(qd * 32) << 16) + col; };
     mbar_wait(&bars[kSFull], 0);
     tc_fence_after();
     if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 1] = global_ns();
-    float* part_m = part;            // [8 warps][NP]
-    float* part_s = part + 8 * NP;   // [8 warps][NP]
-    for (int h0 = 0; h0 < hcols; h0 += 8) {
-      float mx[8], sm[8];
-      for (int e = 0; e < 8; ++e) {
-        mx[e] = -INFINITY;
-        sm[e] = 0.f;
-      }
+    float* part_m = part;                         // [16 warps][NP]
+    float* part_s = part + kComputeWarps * NP;    // [16 warps][NP]
+    for (int c0 = 0; c0 < gcols; c0 += 4) {
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
       for (int t = 0; t < it.tiles; ++t) {
-        float v[8];
-        tmem_ld8(tmem_row(static_cast<uint32_t>(t * NP + hbase + h0)), v);
-        if (t * 128 + qd * 32 + lane >= it.chunk_len) continue;
-        for (int e = 0; e < 8; ++e) {
-          if (v[e] > mx[e]) {
-            sm[e] = sm[e] * __expf(mx[e] - v[e]) + 1.f;
-            mx[e] = v[e];
-          } else {
-            sm[e] += __expf(v[e] - mx[e]);
-          }
-        }
+        float v[4];
+        tmem_ld4(tmem_row(static_cast<uint32_t>(t * NP + gbase + c0)), v);
+        if (t * 128 + qd * 32 + lane < it.chunk_len)
+          for (int e = 0; e < 4; ++e) mx[e] = fmaxf(mx[e], v[e]);
       }
-      for (int e = 0; e < 8; ++e) {
-        float m = mx[e], z = sm[e];
-        for (int o = 16; o > 0; o >>= 1) {
-          const float m2 = __shfl_xor_sync(0xffffffffu, m, o), z2 = __shfl_xor_sync(0xffffffffu, z, o);
-          const float mm = fmaxf(m, m2);
-          z = (mm == -INFINITY) ? 0.f : z * __expf(m - mm) + z2 * __expf(m2 - mm);
-          m = mm;
-        }
-        if (lane == 0) {
-          part_m[cw * NP + hbase + h0 + e] = m;
-          part_s[cw * NP + hbase + h0 + e] = z;
-        }
+      for (int e = 0; e < 4; ++e) {
+        const float m = warp_max(mx[e]);
+        if (lane == 0) part_m[cw * NP + gbase + c0 + e] = m;
       }
     }
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 6] = global_ns();
     named_bar(kBarCompute, kComputeThreads);
     if (tid < H) {
-      const int h = tid, hb = (h / hcols) * 4;
+      const int h = tid, w0 = (h / gcols) * 4;
       float m = -INFINITY;
-      for (int w = 0; w < 4; ++w) m = fmaxf(m, part_m[(hb + w) * NP + h]);
+      for (int w = 0; w < 4; ++w) m = fmaxf(m, part_m[(w0 + w) * NP + h]);
       for (int j = 0; j < it.n_tk; ++j) m = fmaxf(m, stail[j * NP + h]);
-      float z = 0.f;
-      for (int w = 0; w < 4; ++w) {
-        const float mw = part_m[(hb + w) * NP + h];
-        if (mw != -INFINITY) z += part_s[(hb + w) * NP + h] * __expf(mw - m);
-      }
-      for (int j = 0; j < it.n_tk; ++j) z += __expf(stail[j * NP + h] - m);
       m_loc[h] = m;
-      z_loc[h] = z;
     }
     named_bar(kBarCompute, kComputeThreads);
     if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 2] = global_ns();
 
-    // ---- p tiles with the local max (bf16 hi/lo B operand, K-major over tokens)
+    // ---- p tiles with the local max (bf16 hi/lo B operand, K-major over tokens); z from the same pass
+    float zp[gcols];
+#pragma unroll
+    for (int e = 0; e < gcols; ++e) zp[e] = 0.f;
     for (int t = 0; t < it.tiles; ++t) {
       const int buf = t & 1;
       if (t >= 2) mbar_wait(&bars[kPEmpty0 + buf], ((t - 2) >> 1) & 1);
@@ -551,12 +545,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       unsigned char* ptl = pth + 2 * NP * 128;
       const int row = qd * 32 + lane;  // token within the tile
       const bool valid = t * 128 + row < it.chunk_len;
-      for (int h0 = 0; h0 < hcols; h0 += 8) {
-        float v[8];
-        tmem_ld8(tmem_row(static_cast<uint32_t>(t * NP + hbase + h0)), v);
-        for (int e = 0; e < 8; ++e) {
-          const int h = hbase + h0 + e;
+#pragma unroll
+      for (int c0 = 0; c0 < gcols; c0 += 4) {
+        float v[4];
+        tmem_ld4(tmem_row(static_cast<uint32_t>(t * NP + gbase + c0)), v);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int h = gbase + c0 + e;
           const float pv = (valid && h < H) ? __expf(v[e] - m_loc[h]) : 0.f;
+          zp[c0 + e] += pv;
           __nv_bfloat16 hi, lo;
           split_bf16(pv, hi, lo);
           const uint32_t off = (row >> 6) * NP * 128 + sw128_off(h, row & 63);
@@ -568,10 +565,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       named_bar(kBarCompute, kComputeThreads);
       if (tid == 0) mbar_arrive(&bars[kPFull0 + buf]);
     }
+#pragma unroll
+    for (int c0 = 0; c0 < gcols; ++c0) {
+      const float z = warp_sum(zp[c0]);
+      if (lane == 0) part_s[cw * NP + gbase + c0] = z;
+    }
     // tail: local p in place of the logits
     for (int w = tid; w < it.n_tk * H; w += kComputeThreads) {
       const int j = w / H, h = w % H;
       stail[j * NP + h] = __expf(stail[j * NP + h] - m_loc[h]);
+    }
+    named_bar(kBarCompute, kComputeThreads);
+    if (tid < H) {
+      const int h = tid, w0 = (h / gcols) * 4;
+      float z = 0.f;
+      for (int w = 0; w < 4; ++w) z += part_s[(w0 + w) * NP + h];
+      for (int j = 0; j < it.n_tk; ++j) z += stail[j * NP + h];
+      z_loc[h] = z;
     }
     if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 3] = global_ns();
 
@@ -582,11 +592,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* uloc = reinterpret_cast<float*>(smem + L.uloc);
     for (int mt = 0; mt < p.mtiles; ++mt) {
       const int r = mt * 128 + qd * 32 + lane;
-      for (int h0 = 0; h0 < hcols; h0 += 8) {
-        float v[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        if (it.tiles > 0) tmem_ld8(tmem_row(s_cols + static_cast<uint32_t>(mt * NP + hbase + h0)), v);
-        for (int e = 0; e < 8; ++e) {
-          const int h = hbase + h0 + e;
+      for (int c0 = 0; c0 < gcols; c0 += 4) {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (it.tiles > 0) tmem_ld4(tmem_row(s_cols + static_cast<uint32_t>(mt * NP + gbase + c0)), v);
+        for (int e = 0; e < 4; ++e) {
+          const int h = gbase + c0 + e;
           if (h < H && r < p.s.rank_v) uloc[h * L.uloc_stride + r] = v[e];
         }
       }
@@ -655,25 +665,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid < C) mbar_arrive_cluster(&bars[kDone], static_cast<uint32_t>(tid));
 
     // ---- head-averaged attention + importance EMA (importance.cpp:33-65), S re-read from TMEM
-    float* ha_half = part;  // [2][128] (part_m / part_s are dead)
+    float* ha_part = part;  // [4 groups][128] (part_m / part_s are dead)
     const float inv_h = 1.0f / static_cast<float>(H);
     for (int t = 0; t < it.tiles; ++t) {
       const int row = qd * 32 + lane;
       float hsum = 0.f;
-      for (int h0 = 0; h0 < hcols; h0 += 8) {
-        float v[8];
-        tmem_ld8(tmem_row(static_cast<uint32_t>(t * NP + hbase + h0)), v);
-        for (int e = 0; e < 8; ++e) {
-          const int h = hbase + h0 + e;
+      for (int c0 = 0; c0 < gcols; c0 += 4) {
+        float v[4];
+        tmem_ld4(tmem_row(static_cast<uint32_t>(t * NP + gbase + c0)), v);
+        for (int e = 0; e < 4; ++e) {
+          const int h = gbase + c0 + e;
           if (h < H) hsum = fmaf(__expf(v[e] - m_loc[h]), f_me[h], hsum);
         }
       }
-      ha_half[hf * 128 + row] = hsum;
+      ha_part[cg * 128 + row] = hsum;
       named_bar(kBarCompute, kComputeThreads);
       if (tid < 128) {
         const int tk = t * 128 + tid;
         if (tk < it.chunk_len) {
-          const float ha = (ha_half[tid] + ha_half[128 + tid]) * inv_h;
+          const float ha = (ha_part[tid] + ha_part[128 + tid] + ha_part[256 + tid] + ha_part[384 + tid]) * inv_h;
           const long gi = it.c_first + tk;
           if (a.head_avg) a.head_avg[static_cast<long>(b) * (p.s.n_comp + p.s.tail_cap) + gi] = ha;
           if (a.importance)
@@ -744,7 +754,7 @@ FusedPlan plan_fused(const FusedShape& s) {
   const int per_kv = s.H / s.Hkv;
   if (per_kv != 1 && per_kv != 2 && per_kv != 4) return bad("fused path needs 1, 2 or 4 query heads per kv head");
   if (s.D != 128 && s.D != 64) return bad("fused path needs head_dim 64 or 128");
-  if (s.H > 128) return bad("fused path supports up to 128 query heads");
+  if (s.H > 64) return bad("fused path supports up to 64 query heads");
   if (s.rank_k < 1 || s.rank_v < 1) return bad("fused path needs low-rank K and V");
   if (s.ld_left % 8 != 0 || s.ld_left < std::max(s.rank_k, s.rank_v))
     return bad("left-factor stride must be a multiple of 8 and cover both ranks");
@@ -762,9 +772,20 @@ FusedPlan plan_fused(const FusedShape& s) {
   const int cols = p.max_tiles * p.np + p.mtiles * p.np;
   if (cols > 512) return bad("TMEM budget exceeded (raise the cluster size)");
   p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
-  const Smem L = smem_layout(p);
-  p.smem_bytes = L.total;
-  if (p.smem_bytes > 227 * 1024) return bad("shared-memory budget exceeded");
+  p.stages = 4;
+  if (smem_layout(p).total > 227 * 1024) return bad("shared-memory budget exceeded");
+  while (p.stages + 2 <= kMaxStages) {
+    FusedPlan q = p;
+    q.stages = p.stages + 2;
+    if (smem_layout(q).total > 227 * 1024) break;
+    p.stages = q.stages;
+  }
+  if (const char* e = std::getenv("KVP_FUSED_STAGES")) {  // tuning override
+    const int want = std::atoi(e);
+    if (want >= 2 && want <= kMaxStages && want % 2 == 0 && want < p.stages) p.stages = want;
+  }
+  p.box32_only = std::getenv("KVP_FUSED_BOX32") != nullptr;
+  p.smem_bytes = smem_layout(p).total;
   const size_t vs = (static_cast<size_t>(per_kv) * ((s.rank_v + s.tail_cap + 3) & ~3) + 8 * (256 / s.D) * per_kv * s.D) * 4;
   if (vs > 200 * 1024) return bad("vsum weights exceed shared memory");
   p.ok = true;
@@ -780,10 +801,11 @@ size_t fused_workspace_bytes(const FusedShape& s) {
 
 void encode_fused_maps(const FusedShape& s, const void* left_k, const void* left_v, CUtensorMap* maps) {
   const uint64_t rows = static_cast<uint64_t>(s.batch) * s.n_comp;
-  encode_2d(&maps[0], left_k, s.rank_k, rows, static_cast<uint64_t>(s.ld_left) * 2, 64, 32,
-            CU_TENSOR_MAP_SWIZZLE_128B);
-  encode_2d(&maps[1], left_v, s.rank_v, rows, static_cast<uint64_t>(s.ld_left) * 2, 64, 32,
-            CU_TENSOR_MAP_SWIZZLE_128B);
+  const uint64_t ld = static_cast<uint64_t>(s.ld_left) * 2;
+  encode_2d(&maps[0], left_k, s.rank_k, rows, ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  encode_2d(&maps[1], left_v, s.rank_v, rows, ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  encode_2d(&maps[2], left_k, s.rank_k, rows, ld, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+  encode_2d(&maps[3], left_v, s.rank_v, rows, ld, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 template <int PER_KV, int D>
@@ -818,15 +840,22 @@ void launch_stream(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, bool
   }
 }
 
+using CoreFn = void (*)(const FusedPlan, const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
+                       const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, const FusedArgs);
+CoreFn core_for(int np) {
+  switch (np) {
+    case 16: return core_kernel<16>;
+    case 32: return core_kernel<32>;
+    case 48: return core_kernel<48>;
+    default: return core_kernel<64>;
+  }
+}
+
 void launch_fused(const FusedPlan& p, const CUtensorMap* maps, const FusedArgs& a, cudaStream_t st) {
   require(p.ok, KVP_ERR_PARAMETER, p.why);
   launch_stream(p, a, st, true);
-  static size_t attr_bytes = 0;
-  if (attr_bytes < p.smem_bytes) {
-    KVP_CUDA(cudaFuncSetAttribute(core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(p.smem_bytes)));
-    attr_bytes = p.smem_bytes;
-  }
+  auto kernel = core_for(p.np);
+  KVP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_bytes)));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(p.s.batch * p.s.cluster));
   cfg.blockDim = dim3(kThreads);
@@ -839,7 +868,7 @@ void launch_fused(const FusedPlan& p, const CUtensorMap* maps, const FusedArgs& 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  KVP_CUDA(cudaLaunchKernelEx(&cfg, core_kernel, p, maps[0], maps[1], a));
+  KVP_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, maps[0], maps[1], maps[2], maps[3], a));
   KVP_LAUNCHED();
   launch_stream(p, a, st, false);
 }
@@ -856,10 +885,10 @@ int max_active_clusters(const FusedPlan& p) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  KVP_CUDA(cudaFuncSetAttribute(core_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(p.smem_bytes)));
+  auto kernel = core_for(p.np);
+  KVP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_bytes)));
   int n = 0;
-  KVP_CUDA(cudaOccupancyMaxActiveClusters(&n, core_kernel, &cfg));
+  KVP_CUDA(cudaOccupancyMaxActiveClusters(&n, kernel, &cfg));
   return n;
 }
 
@@ -870,26 +899,14 @@ static unsigned long long* g_trace = nullptr;
 extern "C" void kvp_debug_fused_trace(void* dev_buffer) { g_trace = static_cast<unsigned long long*>(dev_buffer); }
 
 namespace {
-// Cluster size: the largest of {8, 4, 2, 1} whose plan fits and that keeps
-// the whole batch in the fewest waves of co-resident clusters.
+// Cluster size: 4 CTAs per instance when the plan fits (measured fastest on
+// B200 for the C2/C5 shapes), else 8, 2, 1.
 int auto_cluster(kvp::FusedShape s) {
-  static std::map<std::tuple<int, int, int, int, int, int, int, int>, int> cache;
-  const auto key = std::make_tuple(s.H, s.Hkv, s.D, s.n_comp, s.rank_k, s.rank_v, s.tail_cap, s.batch);
-  if (auto it = cache.find(key); it != cache.end()) return it->second;
-  int best = 8, best_waves = 1 << 30;
-  for (int c : {8, 4, 2, 1}) {
+  for (int c : {4, 8, 2, 1}) {
     s.cluster = c;
-    const kvp::FusedPlan p = kvp::plan_fused(s);
-    if (!p.ok) continue;
-    const int active = std::max(1, kvp::max_active_clusters(p));
-    const int waves = (s.batch + active - 1) / active;
-    if (waves < best_waves) {
-      best_waves = waves;
-      best = c;
-    }
+    if (kvp::plan_fused(s).ok) return c;
   }
-  cache[key] = best;
-  return best;
+  return 8;
 }
 kvp::FusedShape shape_of(const kvp_fused_desc* d) {
   kvp::FusedShape s{d->heads, d->kv_heads, d->head_dim, d->n_comp, d->rank_k, d->rank_v, d->ld_left,
@@ -932,7 +949,7 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     } else {
       require(d->workspace_bytes >= ws_bytes, KVP_ERR_PARAMETER, "decode_fused: workspace too small");
     }
-    CUtensorMap maps[2];
+    CUtensorMap maps[4];
     encode_fused_maps(s, d->left_k, d->left_v, maps);
     FusedArgs a{};
     a.right_k = static_cast<const __nv_bfloat16*>(d->right_k);

@@ -53,6 +53,8 @@ struct FusedPlan {
   int max_tiles;       // ceil(chunk / 128)
   int tail_max;        // max tail tokens per CTA
   int heads_per_cta;   // query heads per CTA in the U reduce-scatter
+  int stages;          // TMA ring stages (even)
+  bool box32_only;     // tuning: force 32-row TMA boxes
   size_t smem_bytes;
   int tmem_cols;
   bool ok;
@@ -61,7 +63,7 @@ struct FusedPlan {
 
 FusedPlan plan_fused(const FusedShape& s);
 size_t fused_workspace_bytes(const FusedShape& s);
-void encode_fused_maps(const FusedShape& s, const void* left_k, const void* left_v, CUtensorMap* maps /*[2]*/);
+void encode_fused_maps(const FusedShape& s, const void* left_k, const void* left_v, CUtensorMap* maps /*[4]*/);
 void launch_fused(const FusedPlan& p, const CUtensorMap* maps, const FusedArgs& a, cudaStream_t st);
 
 }  // namespace kvp

@@ -30,11 +30,12 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--trace", action="store_true")
+    ap.add_argument("--ld", type=int, default=0)
     args = ap.parse_args()
     c = CONFIGS[args.config]
     B, H, Hkv, D, n, rk, rv, nt, cap = (c[k] for k in ("B", "H", "Hkv", "D", "n", "rk", "rv", "nt", "cap"))
     W = Hkv * D
-    ld = (max(rk, rv) + 7) // 8 * 8
+    ld = args.ld or (max(rk, rv) + 7) // 8 * 8
     dev = "cuda"
     bf = torch.bfloat16
     layers = []
@@ -72,9 +73,11 @@ def main():
         capi.lib().kvp_debug_fused_trace(None)
         capi.lib().kvp_debug_fused_max_clusters.argtypes = [C.POINTER(FusedDesc)]
         print("max active clusters:", capi.lib().kvp_debug_fused_max_clusters(C.byref(layers[0]["desc"])))
-        t = buf.view(B * cl, 16)[:, :6].double().cpu()
+        t = buf.view(B * cl, 16)[:, :11].double().cpu()
+        t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
-        names = ["start", "S ready", "local stats", "p tiles", "U ready", "end"]
+        names = ["start", "S ready", "local stats", "p tiles", "U ready", "end", "stats tmem", "stats bar",
+                 "mma P ok", "mma S done", "prod LV0"]
         rel = (t - t0) / 1000.0
         print("phase (us since first CTA start): median / max over CTAs")
         for k, n_ in enumerate(names):
