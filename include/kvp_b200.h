@@ -187,6 +187,73 @@ size_t kvp_decode_fused_workspace(const kvp_fused_desc* desc);
  * fused kernel's envelope (then use kvp_attend_plan). */
 int kvp_decode_fused(const kvp_fused_desc* desc, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* Device decode engine: the batched serving loop of the synthetic harness   */
+/* (harness.cpp:239-360 run_instance, decoder.cpp:555-617 decode_step).      */
+/* ------------------------------------------------------------------------ */
+
+/* One modality's synthetic cache profile (harness.hpp:20-25 ModalityProfile). */
+typedef struct {
+  int32_t true_rank;
+  int32_t shared_subspace;
+  double spectrum_decay;
+  double noise_floor;
+} kvp_profile;
+
+/* WorkloadSpec + DecodeConfig subset of the serving layout (harness.hpp:27-38,
+ * decoder.hpp:53-75): visual segment factored at rank_k / rank_v right after
+ * prefill (compress_now), textual segment dense, decode tokens join the
+ * textual tail, importance EMA with `alpha`, untiered decompression. */
+typedef struct {
+  int32_t heads, kv_heads, head_dim;
+  int32_t layers, batch;
+  int32_t visual_tokens, textual_tokens, decode_steps;
+  int32_t rank_k, rank_v;
+  double alpha;
+  uint64_t seed;                /* WorkloadSpec.seed (Philox streams, harness.cpp:29-32) */
+  kvp_profile visual, textual;
+  int32_t svd_method;           /* 0 exact, 1 randomized (linalg.hpp:12-19) */
+  uint64_t svd_seed;
+  int32_t svd_oversampling, svd_power_iterations;
+  int32_t factor_init;          /* 0: compaction of the generated K/V; 1: placeholder factors */
+  int32_t cluster;              /* CTAs per instance in the decode core, 0 = auto */
+} kvp_engine_config;
+
+typedef struct {
+  int32_t cluster, rank_k, rank_v, ld_left, tail_cap, steps_taken;
+  double compaction_ms;
+  uint64_t launches_per_step;          /* kernels of this library per decode step */
+  uint64_t weight_bytes_per_step;      /* projection weights read per step */
+  uint64_t factor_bytes_per_step;      /* left + right factors read per step */
+  uint64_t tail_row_bytes;             /* bytes per tail token (K + V, all layers/instances) */
+  uint64_t importance_bytes_per_token; /* fp64 read + write per token, all layers/instances */
+} kvp_engine_info;
+
+/* Device pointers of one layer's state (for tests / inspection). */
+typedef struct {
+  const void *left_k, *left_v, *right_k, *right_v, *tail_k, *tail_v;
+  const double* importance;
+  const void *w_qkv, *w_o;
+  int32_t n_tail;
+} kvp_engine_layer_view;
+
+typedef struct kvp_engine kvp_engine;
+
+int kvp_engine_create(const kvp_engine_config* config, kvp_engine** engine);
+int kvp_engine_destroy(kvp_engine* engine);
+/* Generate the workload on the device (weights, prefill K/V) and compact it. */
+int kvp_engine_prefill(kvp_engine* engine);
+/* One decode step for every instance: x, y are [dev] batch x H*D fp32. */
+int kvp_engine_step(kvp_engine* engine, const float* x, float* y, void* stream);
+/* Same with [host] buffers (pinned for best results): H2D, step, D2H, sync. */
+int kvp_engine_step_host(kvp_engine* engine, const float* x, float* y);
+int kvp_engine_reset_steps(kvp_engine* engine);
+int kvp_engine_get_info(kvp_engine* engine, kvp_engine_info* info);
+int kvp_engine_layer_state(kvp_engine* engine, int32_t layer, kvp_engine_layer_view* view);
+/* Times the attention launches alone (all layers, current tail length) and
+ * reports ms per layer and the algorithmic bytes per layer. */
+int kvp_engine_time_attention(kvp_engine* engine, int32_t iters, double* ms_per_layer, double* bytes_per_layer);
+
 #ifdef __cplusplus
 }
 #endif

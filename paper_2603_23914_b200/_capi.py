@@ -66,6 +66,46 @@ class AttendDesc(C.Structure):
                 ("head_avg_table", C.c_void_p)]
 
 
+class FusedDesc(C.Structure):
+    _fields_ = [("heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("batch", C.c_int32),
+                ("n_comp", C.c_int32), ("rank_k", C.c_int32), ("rank_v", C.c_int32), ("ld_left", C.c_int32),
+                ("tail_cap", C.c_int32), ("n_tail", C.c_int32), ("n_tail_dev", C.c_void_p),
+                ("cluster", C.c_int32), ("context_bf16", C.c_int32),
+                ("left_k", C.c_void_p), ("right_k", C.c_void_p), ("left_v", C.c_void_p), ("right_v", C.c_void_p),
+                ("tail_k", C.c_void_p), ("tail_v", C.c_void_p), ("queries", C.c_void_p),
+                ("importance", C.c_void_p), ("imp_stride", C.c_int64), ("alpha", C.c_double),
+                ("head_avg", C.c_void_p), ("context", C.c_void_p), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t)]
+
+
+class Profile(C.Structure):
+    _fields_ = [("true_rank", C.c_int32), ("shared_subspace", C.c_int32), ("spectrum_decay", C.c_double),
+                ("noise_floor", C.c_double)]
+
+
+class EngineConfig(C.Structure):
+    _fields_ = [("heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("layers", C.c_int32),
+                ("batch", C.c_int32), ("visual_tokens", C.c_int32), ("textual_tokens", C.c_int32),
+                ("decode_steps", C.c_int32), ("rank_k", C.c_int32), ("rank_v", C.c_int32), ("alpha", C.c_double),
+                ("seed", C.c_uint64), ("visual", Profile), ("textual", Profile), ("svd_method", C.c_int32),
+                ("svd_seed", C.c_uint64), ("svd_oversampling", C.c_int32), ("svd_power_iterations", C.c_int32),
+                ("factor_init", C.c_int32), ("cluster", C.c_int32)]
+
+
+class EngineInfo(C.Structure):
+    _fields_ = [("cluster", C.c_int32), ("rank_k", C.c_int32), ("rank_v", C.c_int32), ("ld_left", C.c_int32),
+                ("tail_cap", C.c_int32), ("steps_taken", C.c_int32), ("compaction_ms", C.c_double),
+                ("launches_per_step", C.c_uint64), ("weight_bytes_per_step", C.c_uint64),
+                ("factor_bytes_per_step", C.c_uint64), ("tail_row_bytes", C.c_uint64),
+                ("importance_bytes_per_token", C.c_uint64)]
+
+
+class LayerView(C.Structure):
+    _fields_ = [("left_k", C.c_void_p), ("left_v", C.c_void_p), ("right_k", C.c_void_p), ("right_v", C.c_void_p),
+                ("tail_k", C.c_void_p), ("tail_v", C.c_void_p), ("importance", C.c_void_p), ("w_qkv", C.c_void_p),
+                ("w_o", C.c_void_p), ("n_tail", C.c_int32)]
+
+
 # name -> (restype, argtypes); every symbol include/kvp_b200.h declares.
 SIGNATURES = {
     "kvp_abi_version": (C.c_int, []),
@@ -78,6 +118,17 @@ SIGNATURES = {
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "kvp_update_importance_host": (C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_double]),
     "kvp_assign_groups_host": (C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "kvp_decode_fused": (C.c_int, [C.POINTER(FusedDesc), C.c_void_p]),
+    "kvp_decode_fused_workspace": (C.c_size_t, [C.POINTER(FusedDesc)]),
+    "kvp_engine_create": (C.c_int, [C.POINTER(EngineConfig), C.POINTER(C.c_void_p)]),
+    "kvp_engine_destroy": (C.c_int, [C.c_void_p]),
+    "kvp_engine_prefill": (C.c_int, [C.c_void_p]),
+    "kvp_engine_step": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "kvp_engine_step_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "kvp_engine_reset_steps": (C.c_int, [C.c_void_p]),
+    "kvp_engine_get_info": (C.c_int, [C.c_void_p, C.POINTER(EngineInfo)]),
+    "kvp_engine_layer_state": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(LayerView)]),
+    "kvp_engine_time_attention": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
 }
 
 _lib = None

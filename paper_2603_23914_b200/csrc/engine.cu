@@ -1,0 +1,518 @@
+// Device-resident decode engine: the batched, B200-native equivalent of the
+// reference harness loop (harness.cpp:239-360 run_instance / decode_step per
+// layer, decoder.cpp:555-617) for the serving layout — every instance's
+// visual segment factored (rank_k / rank_v), textual segment a dense tail
+// that grows by one token per step.
+//
+// One decode step = for each layer l:
+//   x (bf16) --GEMM--> [q | k | v]              (decoder.cpp:574-576; cuBLAS, plain GEMM)
+//   append k, v to the tail; new importance 0   (cache.cpp:147-170 append_tokens)
+//   qdots -> cluster core -> vsum               (decoder.cpp:583-601, decode_fused.cu)
+//   ctx (bf16) --GEMM--> x_{l+1}                (decoder.cpp:590)
+// The whole step is captured once into a CUDA graph and replayed; the tail
+// length lives in a device counter so the graph is static.
+#include <cublas_v2.h>
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "compact.cuh"
+#include "decode_fused.cuh"
+#include "engine.cuh"
+#include "philox.cuh"
+
+struct kvp_engine {
+  kvp_engine_config cfg{};
+  int H = 0, Hkv = 0, D = 0, W = 0, HD = 0, L = 0, B = 0, n = 0, t0 = 0, cap = 0, rk = 0, rv = 0, ld = 0;
+  cudaStream_t stream = nullptr;
+  cublasHandle_t blas = nullptr;
+  void* blas_ws = nullptr;
+  // buffers
+  __nv_bfloat16 *wqkv = nullptr, *wo = nullptr;
+  __nv_bfloat16 *lk = nullptr, *lv = nullptr, *rkf = nullptr, *rvf = nullptr, *tk = nullptr, *tv = nullptr;
+  double* imp = nullptr;
+  __nv_bfloat16 *xb = nullptr, *ctx = nullptr;
+  float *qkv = nullptr, *q = nullptr, *xin = nullptr, *xcur = nullptr, *yout = nullptr;
+  int* n_tail_dev = nullptr;
+  void* fused_ws = nullptr;
+  size_t fused_ws_bytes = 0;
+  kvp::FusedPlan plan{};
+  std::vector<CUtensorMap> maps;  // [L][4]
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  double compaction_ms = 0.0;
+  uint64_t launches_per_step = 0;
+  int steps_taken = 0;
+  std::vector<void*> allocations;
+
+  template <typename T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    kvp::cuda_check(cudaMalloc(&p, count * sizeof(T)), "cudaMalloc (engine)");
+    allocations.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~kvp_engine() {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (void* p : allocations) cudaFree(p);
+    if (blas) cublasDestroy(blas);
+    if (stream) cudaStreamDestroy(stream);
+  }
+  size_t left_elems() const { return static_cast<size_t>(B) * n * ld; }
+  size_t right_k_elems() const { return static_cast<size_t>(B) * rk * W; }
+  size_t right_v_elems() const { return static_cast<size_t>(B) * rv * W; }
+  size_t tail_elems() const { return static_cast<size_t>(B) * cap * W; }
+  size_t imp_stride() const { return static_cast<size_t>(n) + cap; }
+};
+
+namespace kvp {
+namespace {
+
+void blas_check(cublasStatus_t s, const char* what) {
+  if (s != CUBLAS_STATUS_SUCCESS) fail(KVP_ERR_CUDA, std::string(what) + ": cuBLAS status " + std::to_string(s));
+}
+
+// W ~ N(0,1) / sqrt(HD) from the reference's weight streams (harness.cpp:138-151):
+// gaussian_matrix(rows, cols, seed, stream_id(1, 0, l, extra)), written into a
+// column block of a wider row-major matrix (W_q | W_k | W_v share one buffer).
+__global__ void gen_weight_kernel(__nv_bfloat16* out, long ld_out, int col0, int rows, int cols, uint64_t seed,
+                                  uint64_t stream, float scale) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<long>(rows) * cols) return;
+  const long r = i / cols, c = i % cols;
+  out[r * ld_out + col0 + c] = __float2bfloat16_rn(static_cast<float>(philox_gaussian(seed, stream, i)) * scale);
+}
+
+// Staged latent-factor model (harness.cpp:82-128): one Philox stream per matrix,
+// consumed as z (T x r, latent i scaled by decay^i), shared loadings
+// (shared x D), per-head loadings (Hkv x (r - shared) x D), then noise (T x W).
+// out[t, h*D + j] = sum_i z[t,i] * load_h[i, j] + noise * g.
+__global__ void latent_direct_kernel(__nv_bfloat16* out, long ld_out, int T, int Hkv, int D, int r, int shared,
+                                     double decay, double noise, uint64_t seed, uint64_t stream) {
+  const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int W = Hkv * D;
+  if (idx >= static_cast<long>(T) * W) return;
+  const int t = static_cast<int>(idx / W), col = static_cast<int>(idx % W), h = col / D, j = col % D;
+  const uint64_t base_s = static_cast<uint64_t>(T) * r;
+  const uint64_t base_h = base_s + static_cast<uint64_t>(shared) * D;
+  const uint64_t base_n = base_h + static_cast<uint64_t>(Hkv) * (r - shared) * D;
+  double acc = 0.0, sc = 1.0;
+  for (int i = 0; i < r; ++i) {
+    const double z = philox_gaussian(seed, stream, static_cast<uint64_t>(t) * r + i) * sc;
+    const double l = i < shared ? philox_gaussian(seed, stream, base_s + static_cast<uint64_t>(i) * D + j)
+                                : philox_gaussian(seed, stream, base_h + (static_cast<uint64_t>(h) * (r - shared) + (i - shared)) * D + j);
+    acc += z * l;
+    sc *= decay;
+  }
+  if (noise > 0.0) acc += noise * philox_gaussian(seed, stream, base_n + static_cast<uint64_t>(t) * W + col);
+  out[static_cast<long>(t) * ld_out + col] = __float2bfloat16_rn(static_cast<float>(acc));
+}
+
+// Placeholder factors for factor_init = 1 (decode-only benchmarking): left
+// rows N(0,1) * 0.98^r, right rows N(0,1)/sqrt(W) (near-orthonormal for W >> R).
+__global__ void synth_factor_kernel(__nv_bfloat16* left, int n, int ld, int rank, __nv_bfloat16* right, int W,
+                                    uint64_t seed, uint64_t stream) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long nl = static_cast<long>(n) * ld, nr = static_cast<long>(rank) * W;
+  if (i < nl) {
+    const int r = static_cast<int>(i % ld);
+    const float v = r < rank ? static_cast<float>(philox_gaussian(seed, stream, i) * pow(0.98, r)) : 0.f;
+    left[i] = __float2bfloat16_rn(v);
+  } else if (i < nl + nr) {
+    const long k = i - nl;
+    right[k] = __float2bfloat16_rn(static_cast<float>(philox_gaussian(seed, stream ^ 0x5A5Aull, k)) * rsqrtf(float(W)));
+  }
+}
+
+__global__ void to_bf16_kernel(const float* in, __nv_bfloat16* out, long n) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __float2bfloat16_rn(in[i]);
+}
+
+__global__ void bump_counter_kernel(int* c) { *c += 1; }
+
+// Split [q | k | v] (fp32, B x (HD + 2W)); q -> q buffer, k/v -> bf16 tail row
+// (n_tail - 1), new token importance 0 (cache.cpp:147-170, importance.cpp:9-14).
+__global__ void append_kernel(const float* qkv, float* q, __nv_bfloat16* tk, __nv_bfloat16* tv, double* imp,
+                              const int* n_tail, int HD, int W, int cap, int n_comp, long imp_stride) {
+  const int b = blockIdx.y;
+  const int row = *n_tail - 1;
+  const float* src = qkv + static_cast<long>(b) * (HD + 2 * W);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HD + 2 * W; i += gridDim.x * blockDim.x) {
+    if (i < HD) {
+      q[static_cast<long>(b) * HD + i] = src[i];
+    } else if (i < HD + W) {
+      tk[(static_cast<long>(b) * cap + row) * W + (i - HD)] = __float2bfloat16_rn(src[i]);
+    } else {
+      tv[(static_cast<long>(b) * cap + row) * W + (i - HD - W)] = __float2bfloat16_rn(src[i]);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) imp[static_cast<long>(b) * imp_stride + n_comp + row] = 0.0;
+}
+
+void launch_1d(long n, auto&& f) {
+  const int threads = 256;
+  const long blocks = (n + threads - 1) / threads;
+  f(static_cast<unsigned>(blocks), threads);
+  KVP_LAUNCHED();
+}
+
+// Row-major C (m x n, fp32) = A (m x k, bf16) * B (k x n, bf16), ldb = n_total.
+void gemm_bf16(kvp_engine* e, int m, int n, int k, const __nv_bfloat16* a, const __nv_bfloat16* b, int ldb,
+               float* c) {
+  const float one = 1.f, zero = 0.f;
+  blas_check(cublasGemmEx(e->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, m, k, &one, b, CUDA_R_16BF, ldb, a, CUDA_R_16BF, k,
+                          &zero, c, CUDA_R_32F, n, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
+             "cublasGemmEx");
+}
+
+FusedArgs fused_args(kvp_engine* e, int l) {
+  FusedArgs a{};
+  const size_t lidx = static_cast<size_t>(l);
+  a.right_k = e->rkf + lidx * e->right_k_elems();
+  a.right_v = e->rvf + lidx * e->right_v_elems();
+  a.tail_k = e->tk + lidx * e->tail_elems();
+  a.tail_v = e->tv + lidx * e->tail_elems();
+  a.n_tail_dev = e->n_tail_dev;
+  a.n_tail = 0;
+  a.q = e->q;
+  a.importance = e->imp + lidx * e->B * e->imp_stride();
+  a.imp_stride = static_cast<long>(e->imp_stride());
+  a.ema_decay = std::pow(e->cfg.alpha, 1.0);
+  a.ema_blend = 1.0 - a.ema_decay;
+  a.head_avg = nullptr;
+  a.ctx_out = e->ctx;
+  a.ctx_bf16 = 1;
+  a.ws_pimg = static_cast<unsigned char*>(e->fused_ws);
+  a.ws_tail = reinterpret_cast<float*>(a.ws_pimg + static_cast<size_t>(e->B) * 2 * e->plan.kpk * e->plan.np * 128);
+  a.ws_u = a.ws_tail + static_cast<size_t>(e->B) * e->H * e->cap;
+  a.trace = nullptr;
+  return a;
+}
+
+// One decode step over all layers, enqueued on e->stream (graph-capturable).
+void enqueue_step(kvp_engine* e) {
+  cudaStream_t s = e->stream;
+  bump_counter_kernel<<<1, 1, 0, s>>>(e->n_tail_dev);
+  KVP_LAUNCHED();
+  const long nx = static_cast<long>(e->B) * e->HD;
+  const float* x = e->xin;
+  for (int l = 0; l < e->L; ++l) {
+    launch_1d(nx, [&](unsigned g, int t) { to_bf16_kernel<<<g, t, 0, s>>>(x, e->xb, nx); });
+    const int nqkv = e->HD + 2 * e->W;
+    gemm_bf16(e, e->B, nqkv, e->HD, e->xb, e->wqkv + static_cast<size_t>(l) * e->HD * nqkv, nqkv, e->qkv);
+    append_kernel<<<dim3(16, e->B), 256, 0, s>>>(e->qkv, e->q, e->tk + static_cast<size_t>(l) * e->tail_elems(),
+                                                  e->tv + static_cast<size_t>(l) * e->tail_elems(),
+                                                  e->imp + static_cast<size_t>(l) * e->B * e->imp_stride(), e->n_tail_dev,
+                                                  e->HD, e->W, e->cap, e->n, static_cast<long>(e->imp_stride()));
+    KVP_LAUNCHED();
+    launch_fused(e->plan, &e->maps[static_cast<size_t>(l) * 4], fused_args(e, l), s);
+    float* out = (l + 1 == e->L) ? e->yout : e->xcur;
+    gemm_bf16(e, e->B, e->HD, e->HD, e->ctx, e->wo + static_cast<size_t>(l) * e->HD * e->HD, e->HD, out);
+    x = out;
+  }
+}
+
+void build_graph(kvp_engine* e) {
+  if (e->graph_exec) return;
+  const uint64_t before = kvp_launch_count();
+  KVP_CUDA(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    enqueue_step(e);
+  } catch (...) {
+    cudaGraph_t g;
+    cudaStreamEndCapture(e->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  KVP_CUDA(cudaStreamEndCapture(e->stream, &e->graph));
+  KVP_CUDA(cudaGraphInstantiate(&e->graph_exec, e->graph, 0));
+  // kernels of ours per step (cuBLAS GEMMs excluded from the count)
+  e->launches_per_step = kvp_launch_count() - before;
+}
+
+}  // namespace
+}  // namespace kvp
+
+using namespace kvp;
+
+extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
+  return guarded([&] {
+    require(c && out, KVP_ERR_PARAMETER, "engine: null argument");
+    require(c->heads > 0 && c->kv_heads > 0 && c->head_dim > 0, KVP_ERR_PARAMETER,
+            "HeadGeometry: head counts and head_dim must be positive");
+    require(c->heads % c->kv_heads == 0, KVP_ERR_PARAMETER, "HeadGeometry: num_kv_heads must divide num_query_heads");
+    require(c->layers >= 1 && c->batch >= 1, KVP_ERR_PARAMETER, "WorkloadSpec: layers and batch must be >= 1");
+    require(c->visual_tokens >= 1 && c->rank_k >= 1 && c->rank_v >= 1, KVP_ERR_PARAMETER,
+            "engine: the serving layout needs a factored visual segment");
+    require(c->alpha >= 0.0 && c->alpha <= 1.0, KVP_ERR_PARAMETER, "DecodeConfig: alpha must be in [0, 1]");
+    auto e = std::make_unique<kvp_engine>();
+    e->cfg = *c;
+    e->H = c->heads;
+    e->Hkv = c->kv_heads;
+    e->D = c->head_dim;
+    e->W = e->Hkv * e->D;
+    e->HD = e->H * e->D;
+    e->L = c->layers;
+    e->B = c->batch;
+    e->n = c->visual_tokens;
+    e->t0 = c->textual_tokens;
+    e->cap = c->textual_tokens + c->decode_steps;
+    e->rk = std::min(c->rank_k, std::min(e->n, e->W));  // compress_segment clamp (compressor.cpp:46-59)
+    e->rv = std::min(c->rank_v, std::min(e->n, e->W));
+    e->ld = (std::max(e->rk, e->rv) + 63) / 64 * 64;
+    FusedShape fs{e->H, e->Hkv, e->D, e->n, e->rk, e->rv, e->ld, e->cap, e->B, c->cluster};
+    if (fs.cluster <= 0) {
+      for (int cl : {4, 8, 2, 1}) {
+        fs.cluster = cl;
+        if (plan_fused(fs).ok) break;
+      }
+    }
+    e->plan = plan_fused(fs);
+    require(e->plan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->plan.why).c_str());
+    KVP_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    blas_check(cublasCreate(&e->blas), "cublasCreate");
+    blas_check(cublasSetStream(e->blas, e->stream), "cublasSetStream");
+    const size_t blas_ws = 32u << 20;
+    e->blas_ws = e->alloc<char>(blas_ws);
+    blas_check(cublasSetWorkspace(e->blas, e->blas_ws, blas_ws), "cublasSetWorkspace");
+    const size_t L = e->L;
+    e->wqkv = e->alloc<__nv_bfloat16>(L * e->HD * (e->HD + 2 * e->W));
+    e->wo = e->alloc<__nv_bfloat16>(L * e->HD * e->HD);
+    e->lk = e->alloc<__nv_bfloat16>(L * e->left_elems());
+    e->lv = e->alloc<__nv_bfloat16>(L * e->left_elems());
+    e->rkf = e->alloc<__nv_bfloat16>(L * e->right_k_elems());
+    e->rvf = e->alloc<__nv_bfloat16>(L * e->right_v_elems());
+    e->tk = e->alloc<__nv_bfloat16>(L * e->tail_elems());
+    e->tv = e->alloc<__nv_bfloat16>(L * e->tail_elems());
+    e->imp = e->alloc<double>(L * e->B * e->imp_stride());
+    e->xb = e->alloc<__nv_bfloat16>(static_cast<size_t>(e->B) * e->HD);
+    e->ctx = e->alloc<__nv_bfloat16>(static_cast<size_t>(e->B) * e->HD);
+    e->qkv = e->alloc<float>(static_cast<size_t>(e->B) * (e->HD + 2 * e->W));
+    e->q = e->alloc<float>(static_cast<size_t>(e->B) * e->HD);
+    e->xin = e->alloc<float>(static_cast<size_t>(e->B) * e->HD);
+    e->xcur = e->alloc<float>(static_cast<size_t>(e->B) * e->HD);
+    e->yout = e->alloc<float>(static_cast<size_t>(e->B) * e->HD);
+    e->n_tail_dev = e->alloc<int>(1);
+    e->fused_ws_bytes = fused_workspace_bytes(fs);
+    e->fused_ws = e->alloc<char>(e->fused_ws_bytes);
+    KVP_CUDA(cudaMemset(e->fused_ws, 0, e->fused_ws_bytes));
+    e->maps.resize(L * 4);
+    for (size_t l = 0; l < L; ++l)
+      encode_fused_maps(fs, e->lk + l * e->left_elems(), e->lv + l * e->left_elems(), &e->maps[l * 4]);
+    *out = e.release();
+  });
+}
+
+extern "C" int kvp_engine_destroy(kvp_engine* e) {
+  return guarded([&] { delete e; });
+}
+
+extern "C" int kvp_engine_prefill(kvp_engine* e) {
+  return guarded([&] {
+    require(e != nullptr, KVP_ERR_PARAMETER, "engine: null");
+    cudaStream_t s = e->stream;
+    const uint64_t seed = e->cfg.seed;
+    const float wscale = 1.0f / std::sqrt(static_cast<float>(e->HD));
+    const int nqkv = e->HD + 2 * e->W;
+    for (int l = 0; l < e->L; ++l) {
+      __nv_bfloat16* wqkv = e->wqkv + static_cast<size_t>(l) * e->HD * nqkv;
+      const struct { int col0, cols, extra; } parts[3] = {{0, e->HD, 0}, {e->HD, e->W, 1}, {e->HD + e->W, e->W, 2}};
+      for (const auto& pt : parts)
+        launch_1d(static_cast<long>(e->HD) * pt.cols, [&](unsigned g, int t) {
+          gen_weight_kernel<<<g, t, 0, s>>>(wqkv, nqkv, pt.col0, e->HD, pt.cols, seed, stream_id(1, 0, l, pt.extra),
+                                            wscale);
+        });
+      launch_1d(static_cast<long>(e->HD) * e->HD, [&](unsigned g, int t) {
+        gen_weight_kernel<<<g, t, 0, s>>>(e->wo + static_cast<size_t>(l) * e->HD * e->HD, e->HD, 0, e->HD, e->HD, seed,
+                                          stream_id(1, 0, l, 3), wscale);
+      });
+    }
+    // textual prefill -> dense tails (harness.cpp:158-167, profile harness.hpp:33)
+    KVP_CUDA(cudaMemsetAsync(e->tk, 0, sizeof(__nv_bfloat16) * e->L * e->tail_elems(), s));
+    KVP_CUDA(cudaMemsetAsync(e->tv, 0, sizeof(__nv_bfloat16) * e->L * e->tail_elems(), s));
+    if (e->t0 > 0) {
+      for (int l = 0; l < e->L; ++l)
+        for (int b = 0; b < e->B; ++b)
+          for (int kind = 0; kind < 2; ++kind) {
+            __nv_bfloat16* dst = (kind == 0 ? e->tk : e->tv) + static_cast<size_t>(l) * e->tail_elems() +
+                                 static_cast<size_t>(b) * e->cap * e->W;
+            const auto& pr = e->cfg.textual;
+            launch_1d(static_cast<long>(e->t0) * e->W, [&](unsigned g, int t) {
+              latent_direct_kernel<<<g, t, 0, s>>>(dst, e->W, e->t0, e->Hkv, e->D, pr.true_rank,
+                                                   std::min(pr.shared_subspace, pr.true_rank), pr.spectrum_decay,
+                                                   pr.noise_floor, seed, stream_id(2, b, l, 2 + kind));
+            });
+          }
+    }
+    // visual prefill -> factored block (compaction, or placeholder factors)
+    cudaEvent_t e0, e1;
+    KVP_CUDA(cudaEventCreate(&e0));
+    KVP_CUDA(cudaEventCreate(&e1));
+    KVP_CUDA(cudaEventRecord(e0, s));
+    if (e->cfg.factor_init == 1) {
+      for (int l = 0; l < e->L; ++l)
+        for (int b = 0; b < e->B; ++b)
+          for (int kind = 0; kind < 2; ++kind) {
+            const int rank = kind == 0 ? e->rk : e->rv;
+            __nv_bfloat16* left = (kind == 0 ? e->lk : e->lv) + static_cast<size_t>(l) * e->left_elems() +
+                                  static_cast<size_t>(b) * e->n * e->ld;
+            __nv_bfloat16* right = (kind == 0 ? e->rkf + static_cast<size_t>(l) * e->right_k_elems()
+                                              : e->rvf + static_cast<size_t>(l) * e->right_v_elems()) +
+                                   static_cast<size_t>(b) * rank * e->W;
+            launch_1d(static_cast<long>(e->n) * e->ld + static_cast<long>(rank) * e->W, [&](unsigned g, int t) {
+              synth_factor_kernel<<<g, t, 0, s>>>(left, e->n, e->ld, rank, right, e->W, seed, stream_id(2, b, l, kind));
+            });
+          }
+    } else {
+      compact_visual(e);
+    }
+    KVP_CUDA(cudaEventRecord(e1, s));
+    KVP_CUDA(cudaMemsetAsync(e->imp, 0, sizeof(double) * e->L * e->B * e->imp_stride(), s));
+    KVP_CUDA(cudaMemcpyAsync(e->n_tail_dev, &e->t0, sizeof(int), cudaMemcpyHostToDevice, s));
+    KVP_CUDA(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    KVP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    e->compaction_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    e->steps_taken = 0;
+  });
+}
+
+extern "C" int kvp_engine_step(kvp_engine* e, const float* x_dev, float* y_dev, void* stream) {
+  return guarded([&] {
+    require(e != nullptr, KVP_ERR_PARAMETER, "engine: null");
+    require(e->steps_taken < e->cfg.decode_steps, KVP_ERR_PARAMETER, "engine: tail capacity exhausted (decode_steps)");
+    build_graph(e);
+    cudaStream_t caller = as_stream(stream);
+    const size_t bytes = sizeof(float) * e->B * e->HD;
+    // order the engine stream after the caller's work, run, and hand back
+    cudaEvent_t ev;
+    KVP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    KVP_CUDA(cudaEventRecord(ev, caller));
+    KVP_CUDA(cudaStreamWaitEvent(e->stream, ev, 0));
+    KVP_CUDA(cudaMemcpyAsync(e->xin, x_dev, bytes, cudaMemcpyDeviceToDevice, e->stream));
+    KVP_CUDA(cudaGraphLaunch(e->graph_exec, e->stream));
+    KVP_CUDA(cudaMemcpyAsync(y_dev, e->yout, bytes, cudaMemcpyDeviceToDevice, e->stream));
+    KVP_CUDA(cudaEventRecord(ev, e->stream));
+    KVP_CUDA(cudaStreamWaitEvent(caller, ev, 0));
+    KVP_CUDA(cudaEventDestroy(ev));
+    note_launch(e->launches_per_step);
+    ++e->steps_taken;
+  });
+}
+
+extern "C" int kvp_engine_step_host(kvp_engine* e, const float* x_host, float* y_host) {
+  return guarded([&] {
+    require(e != nullptr, KVP_ERR_PARAMETER, "engine: null");
+    require(e->steps_taken < e->cfg.decode_steps, KVP_ERR_PARAMETER, "engine: tail capacity exhausted (decode_steps)");
+    build_graph(e);
+    const size_t bytes = sizeof(float) * e->B * e->HD;
+    KVP_CUDA(cudaMemcpyAsync(e->xin, x_host, bytes, cudaMemcpyHostToDevice, e->stream));
+    KVP_CUDA(cudaGraphLaunch(e->graph_exec, e->stream));
+    KVP_CUDA(cudaMemcpyAsync(y_host, e->yout, bytes, cudaMemcpyDeviceToHost, e->stream));
+    KVP_CUDA(cudaStreamSynchronize(e->stream));
+    note_launch(e->launches_per_step);
+    ++e->steps_taken;
+  });
+}
+
+extern "C" int kvp_engine_reset_steps(kvp_engine* e) {
+  return guarded([&] {
+    require(e != nullptr, KVP_ERR_PARAMETER, "engine: null");
+    KVP_CUDA(cudaMemcpyAsync(e->n_tail_dev, &e->t0, sizeof(int), cudaMemcpyHostToDevice, e->stream));
+    KVP_CUDA(cudaStreamSynchronize(e->stream));
+    e->steps_taken = 0;
+  });
+}
+
+extern "C" int kvp_engine_get_info(kvp_engine* e, kvp_engine_info* info) {
+  return guarded([&] {
+    require(e && info, KVP_ERR_PARAMETER, "engine: null argument");
+    std::memset(info, 0, sizeof(*info));
+    info->cluster = e->plan.s.cluster;
+    info->rank_k = e->rk;
+    info->rank_v = e->rv;
+    info->ld_left = e->ld;
+    info->tail_cap = e->cap;
+    info->steps_taken = e->steps_taken;
+    info->compaction_ms = e->compaction_ms;
+    info->launches_per_step = e->launches_per_step;
+    const double s = 2.0;  // bf16
+    const double nt_avg = e->t0 + 1;  // first step; callers scale with steps_taken
+    (void)nt_avg;
+    info->weight_bytes_per_step =
+        static_cast<uint64_t>(s * e->L * (static_cast<double>(e->HD) * (e->HD + 2 * e->W) + static_cast<double>(e->HD) * e->HD));
+    info->factor_bytes_per_step = static_cast<uint64_t>(
+        s * e->L * e->B * (static_cast<double>(e->n) * (e->rk + e->rv) + static_cast<double>(e->rk + e->rv) * e->W));
+    info->tail_row_bytes = static_cast<uint64_t>(s * e->L * e->B * 2.0 * e->W);  // per tail token, K + V
+    info->importance_bytes_per_token = static_cast<uint64_t>(16.0 * e->L * e->B);
+  });
+}
+
+extern "C" int kvp_engine_layer_state(kvp_engine* e, int layer, kvp_engine_layer_view* v) {
+  return guarded([&] {
+    require(e && v, KVP_ERR_PARAMETER, "engine: null argument");
+    require(layer >= 0 && layer < e->L, KVP_ERR_PARAMETER, "engine: layer out of range");
+    const size_t l = layer;
+    v->left_k = e->lk + l * e->left_elems();
+    v->left_v = e->lv + l * e->left_elems();
+    v->right_k = e->rkf + l * e->right_k_elems();
+    v->right_v = e->rvf + l * e->right_v_elems();
+    v->tail_k = e->tk + l * e->tail_elems();
+    v->tail_v = e->tv + l * e->tail_elems();
+    v->importance = e->imp + l * e->B * e->imp_stride();
+    v->w_qkv = e->wqkv + l * e->HD * (e->HD + 2 * e->W);
+    v->w_o = e->wo + l * e->HD * e->HD;
+    int nt = 0;
+    KVP_CUDA(cudaMemcpy(&nt, e->n_tail_dev, sizeof(int), cudaMemcpyDeviceToHost));
+    v->n_tail = nt;
+  });
+}
+
+// Attention-only timing (the roofline numerator): qdots + core + vsum for
+// every layer at the current tail length, captured as a graph and replayed
+// `iters` times, CUDA events on the engine stream.  Mutates importance only.
+extern "C" int kvp_engine_time_attention(kvp_engine* e, int32_t iters, double* ms_per_layer,
+                                         double* bytes_per_layer) {
+  return guarded([&] {
+    require(e && ms_per_layer && bytes_per_layer && iters > 0, KVP_ERR_PARAMETER, "engine: bad argument");
+    cudaStream_t s = e->stream;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    KVP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    for (int l = 0; l < e->L; ++l) launch_fused(e->plan, &e->maps[static_cast<size_t>(l) * 4], fused_args(e, l), s);
+    KVP_CUDA(cudaStreamEndCapture(s, &g));
+    KVP_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    KVP_CUDA(cudaGraphLaunch(ge, s));  // warm-up
+    cudaEvent_t e0, e1;
+    KVP_CUDA(cudaEventCreate(&e0));
+    KVP_CUDA(cudaEventCreate(&e1));
+    KVP_CUDA(cudaEventRecord(e0, s));
+    for (int i = 0; i < iters; ++i) KVP_CUDA(cudaGraphLaunch(ge, s));
+    KVP_CUDA(cudaEventRecord(e1, s));
+    KVP_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    KVP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    note_launch(static_cast<uint64_t>(iters + 1) * e->L * 3);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    int nt = 0;
+    KVP_CUDA(cudaMemcpy(&nt, e->n_tail_dev, sizeof(int), cudaMemcpyDeviceToHost));
+    *ms_per_layer = ms / (static_cast<double>(iters) * e->L);
+    // s*[n*(Rk+Rv) + (Rk+Rv)*W + 2*T_uc*W] + 16*T per instance (append excluded)
+    const double per = 2.0 * (static_cast<double>(e->n) * (e->rk + e->rv) + static_cast<double>(e->rk + e->rv) * e->W +
+                              2.0 * nt * e->W) +
+                       16.0 * (e->n + nt);
+    *bytes_per_layer = per * e->B;
+  });
+}
