@@ -143,8 +143,17 @@ int kvp_assign_groups_host(int32_t n, const double* scores, int32_t n_groups, co
 /* Fused serving kernel: bf16 compressed cache, T_q = 1, batched instances.  */
 /* ------------------------------------------------------------------------ */
 
+/* Left factors live in the packed layout kvp_pack_left produces: per
+ * instance, per 128-token tile, per 64-rank panel one contiguous 16 KB block
+ * (128 rows of 128 B, 16 B chunks XOR-swizzled by row % 8 — the tcgen05
+ * SWIZZLE_128B K-major operand layout), zero padded.  One bulk copy per block
+ * feeds the tensor cores. */
+size_t kvp_packed_left_bytes(int32_t batch, int32_t n, int32_t rank);
+/* Row-major [batch][n][ld] bf16 left factor -> packed layout. */
+int kvp_pack_left(const void* src, int64_t ld, int32_t batch, int32_t n, int32_t rank, void* dst, void* stream);
+
 /* One layer of a batch of caches in the serving layout: every instance holds
- * one factored block of n_comp tokens (left_k/left_v: [batch][n_comp][ld_left],
+ * one factored block of n_comp tokens (left_k/left_v packed, see above;
  * right_k: [batch][rank_k][W], right_v: [batch][rank_v][W]) and a dense tail
  * (tail_k/tail_v: [batch][tail_cap][W], n_tail rows valid — read from
  * n_tail_dev when non-NULL so the call can live in a CUDA graph).  This is
@@ -155,12 +164,12 @@ int kvp_assign_groups_host(int32_t n, const double* scores, int32_t n_groups, co
  * (importance.cpp:33-65) over [compressed..., tail...] columns. */
 typedef struct {
   int32_t heads, kv_heads, head_dim, batch;
-  int32_t n_comp, rank_k, rank_v, ld_left;
+  int32_t n_comp, rank_k, rank_v, reserved;
   int32_t tail_cap, n_tail;
   const int32_t* n_tail_dev;    /* [dev] nullable */
   int32_t cluster;              /* CTAs per instance, 0 = auto */
   int32_t context_bf16;         /* 1: context is bf16, 0: fp32 */
-  const void* left_k;           /* [dev] bf16 */
+  const void* left_k;           /* [dev] packed (kvp_pack_left) */
   const void* right_k;
   const void* left_v;
   const void* right_v;

@@ -68,7 +68,7 @@ class AttendDesc(C.Structure):
 
 class FusedDesc(C.Structure):
     _fields_ = [("heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("batch", C.c_int32),
-                ("n_comp", C.c_int32), ("rank_k", C.c_int32), ("rank_v", C.c_int32), ("ld_left", C.c_int32),
+                ("n_comp", C.c_int32), ("rank_k", C.c_int32), ("rank_v", C.c_int32), ("reserved", C.c_int32),
                 ("tail_cap", C.c_int32), ("n_tail", C.c_int32), ("n_tail_dev", C.c_void_p),
                 ("cluster", C.c_int32), ("context_bf16", C.c_int32),
                 ("left_k", C.c_void_p), ("right_k", C.c_void_p), ("left_v", C.c_void_p), ("right_v", C.c_void_p),
@@ -118,6 +118,8 @@ SIGNATURES = {
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "kvp_update_importance_host": (C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_double]),
     "kvp_assign_groups_host": (C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "kvp_packed_left_bytes": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
+    "kvp_pack_left": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "kvp_decode_fused": (C.c_int, [C.POINTER(FusedDesc), C.c_void_p]),
     "kvp_decode_fused_workspace": (C.c_size_t, [C.POINTER(FusedDesc)]),
     "kvp_engine_create": (C.c_int, [C.POINTER(EngineConfig), C.POINTER(C.c_void_p)]),

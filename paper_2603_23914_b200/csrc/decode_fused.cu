@@ -55,6 +55,10 @@ constexpr int kComputeWarps = 16;
 constexpr uint32_t kBarCompute = 1;  // named barrier id for the compute warps
 constexpr int kTailMax = 96;
 constexpr int kStreamThreads = 256;  // qdots / vsum blocks
+constexpr int kStreamWarps = kStreamThreads / 32;
+#ifndef QD_UNROLL
+#define QD_UNROLL 1
+#endif
 
 struct Smem {
   uint32_t ring, phi, plo, pt, stail, part, stats, imps, bars, tslot, total;
@@ -103,7 +107,7 @@ enum Bar : int {
 
 struct Items {
   int lk0, lv0, total;
-  int n_tk, tiles, chunk_len, c_first, t_first;
+  int n_tk, tiles, tile0, chunk_len, c_first, t_first;
 };
 
 __device__ __forceinline__ Items make_items(const FusedPlan& p, int c, int n_tail) {
@@ -112,9 +116,10 @@ __device__ __forceinline__ Items make_items(const FusedPlan& p, int c, int n_tai
   const int tail_per = (n_tail + C - 1) / C;
   it.t_first = c * tail_per;
   it.n_tk = max(0, min(n_tail, it.t_first + tail_per) - it.t_first);
-  it.c_first = c * p.chunk;
-  it.chunk_len = max(0, min(p.s.n_comp, it.c_first + p.chunk) - it.c_first);
-  it.tiles = (it.chunk_len + 127) / 128;
+  it.tile0 = c * p.max_tiles;
+  it.tiles = max(0, min(p.ntiles, it.tile0 + p.max_tiles) - it.tile0);
+  it.c_first = it.tile0 * 128;
+  it.chunk_len = max(0, min(p.s.n_comp - it.c_first, it.tiles * 128));
   // ring items (MMA operands only): left_k panels, even-pad, left_v panels
   it.lk0 = 0;
   const int after_lk = it.tiles * p.kpk;
@@ -170,21 +175,42 @@ __device__ __forceinline__ void unpack8(const uint4& raw, float (&v)[8]) {
 // ============================================================================
 template <int PER_KV, int D>
 __global__ void __launch_bounds__(kStreamThreads) qdots_kernel(const FusedPlan p, const FusedArgs a) {
-  constexpr int LPH = D / 8, RPI = 32 / LPH;
+  // A group of LPH = D/8 lanes covers one row segment (D bf16, one kv-head
+  // slice); each lane owns one 16-byte chunk and keeps its 8 query values in
+  // registers.  A group walks blocks of 8 consecutive rows: 8 independent
+  // 16-byte loads in flight per lane, one butterfly transpose-reduction
+  // (8 values over LPH lanes in log2(LPH) rounds), and the 8 results land as
+  // one 16-byte chunk of the swizzled P operand image (k = 8 consecutive ranks).
+  constexpr int LPH = D / 8, GPW = 32 / LPH;  // lanes per row segment, groups per warp
   const int g = blockIdx.x, b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = lane / LPH, gl = lane % LPH;
   const int H = p.s.H, W = p.s.Hkv * D;
   const int n_tail = a.n_tail_dev ? *a.n_tail_dev : a.n_tail;
   const int rk = p.s.rank_k, rows = rk + n_tail;
-  const int col8 = (lane % LPH) * 8, rsub = lane / LPH;
   const float scale = rsqrtf(static_cast<float>(D));
   float qv[PER_KV][8];
 #pragma unroll
   for (int y = 0; y < PER_KV; ++y)
 #pragma unroll
-    for (int e = 0; e < 8; ++e) qv[y][e] = a.q[static_cast<long>(b) * H * D + (g * PER_KV + y) * D + col8 + e] * scale;
-  const __nv_bfloat16* rkb = a.right_k + static_cast<long>(b) * rk * W + g * D + col8;
-  const __nv_bfloat16* tkb = a.tail_k + static_cast<long>(b) * p.s.tail_cap * W + g * D + col8;
+    for (int e = 0; e < 8; ++e)
+      qv[y][e] = a.q[static_cast<long>(b) * a.q_stride + (g * PER_KV + y) * D + gl * 8 + e] * scale;
+  const __nv_bfloat16* rkb = a.right_k + static_cast<long>(b) * rk * W + g * D + gl * 8;
+  const __nv_bfloat16* tkb = a.tail_k + static_cast<long>(b) * p.s.tail_cap * W + g * D + gl * 8;
+  if (a.append_kv) {  // the new token's k, v (this block's kv-head slice) -> tail row n_tail - 1
+    const float* src = a.q + static_cast<long>(b) * a.q_stride + static_cast<long>(H) * D + g * D;
+    const long row = static_cast<long>(b) * p.s.tail_cap + (n_tail - 1);
+    __nv_bfloat16* tk = const_cast<__nv_bfloat16*>(a.tail_k) + row * W + g * D;
+    __nv_bfloat16* tv = const_cast<__nv_bfloat16*>(a.tail_v) + row * W + g * D;
+    for (int i = threadIdx.x; i < D; i += kStreamThreads) {
+      tk[i] = __float2bfloat16_rn(src[i]);
+      tv[i] = __float2bfloat16_rn(src[W + i]);
+    }
+    if (g == 0 && threadIdx.x == 0 && a.importance)
+      a.importance[static_cast<long>(b) * a.imp_stride + p.s.n_comp + n_tail - 1] = 0.0;
+    __threadfence_block();
+    __syncthreads();
+  }
   const int NP = p.np;
   const uint32_t plane = static_cast<uint32_t>(p.kpk) * NP * 128;  // bytes of one (hi or lo) operand
   unsigned char* pimg = a.ws_pimg + static_cast<size_t>(b) * 2 * plane;
@@ -203,40 +229,83 @@ __global__ void __launch_bounds__(kStreamThreads) qdots_kernel(const FusedPlan p
       *reinterpret_cast<__nv_bfloat16*>(pimg + off) = __float2bfloat16_rn(0.f);
       *reinterpret_cast<__nv_bfloat16*>(pimg + plane + off) = __float2bfloat16_rn(0.f);
     }
-  constexpr int U = 8;
-  const int stride = 8 * RPI;  // rows advanced per warp-instruction round across the block
-  for (int r0 = warp * RPI + rsub; r0 < rows; r0 += U * stride) {
-    uint4 raw[U];
+  const int nblk = (rows + 7) / 8;
+  const int gid = warp * GPW + grp, ngroups = (kStreamThreads / 32) * GPW;
+  constexpr int UNR = QD_UNROLL;  // 8-row blocks in flight per group
+  for (int blk0 = gid; blk0 < nblk; blk0 += UNR * ngroups) {
+    uint4 rawb[UNR][8];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int r = r0 + u * stride;
-      if (r < rows) raw[u] = ldg_stream(r < rk ? rkb + static_cast<long>(r) * W : tkb + static_cast<long>(r - rk) * W);
-    }
+    for (int ub = 0; ub < UNR; ++ub)
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int r = r0 + u * stride;
-      float v[8];
-      unpack8(raw[u], v);
+      for (int u = 0; u < 8; ++u) {
+        // unconditional load of a clamped row (no select right after the load, so
+        // all loads stay in flight); rows >= `rows` are discarded at emit
+        const int r = min((blk0 + ub * ngroups) * 8 + u, rows - 1);
+        rawb[ub][u] = ldg_stream(r < rk ? rkb + static_cast<long>(r) * W : tkb + static_cast<long>(r - rk) * W);
+      }
 #pragma unroll
-      for (int y = 0; y < PER_KV; ++y) {
-        float acc = v[0] * qv[y][0];
+    for (int ub = 0; ub < UNR; ++ub) {
+    const int blk = blk0 + ub * ngroups;
+    if (blk >= nblk) break;
+    const int r0 = blk * 8;
+    const uint4* raw = rawb[ub];
 #pragma unroll
-        for (int e = 1; e < 8; ++e) acc = fmaf(v[e], qv[y][e], acc);
+    for (int y = 0; y < PER_KV; ++y) {
+      float acc[8];
 #pragma unroll
-        for (int o = LPH / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if ((lane % LPH) == 0 && r < rows) {
-          const int h = g * PER_KV + y;
-          if (r < rk) {
-            __nv_bfloat16 hi, lo;
-            split_bf16(acc, hi, lo);
-            const uint32_t off = (r >> 6) * NP * 128 + sw128_off(h, r & 63);
-            *reinterpret_cast<__nv_bfloat16*>(pimg + off) = hi;
-            *reinterpret_cast<__nv_bfloat16*>(pimg + plane + off) = lo;
-          } else {
-            tout[static_cast<long>(h) * p.s.tail_cap + (r - rk)] = acc;
+      for (int u = 0; u < 8; ++u) {
+        float v[8];
+        unpack8(raw[u], v);
+        float t = v[0] * qv[y][0];
+#pragma unroll
+        for (int e = 1; e < 8; ++e) t = fmaf(v[e], qv[y][e], t);
+        acc[u] = t;
+      }
+      // butterfly transpose-reduction of acc[0..7] across the LPH lanes of the group:
+      // after the rounds, lane gl holds the full dot of row r0 + (gl % 8).
+      int n = 8;
+#pragma unroll
+      for (int o = LPH / 2; o >= 1; o >>= 1) {
+        if (n > 1) {
+          const bool upper = (gl & o) != 0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (i >= n / 2) break;
+            const float send = upper ? acc[i] : acc[i + n / 2];
+            const float keep = upper ? acc[i + n / 2] : acc[i];
+            acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
           }
+          n /= 2;
+        } else {
+          acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], o);
         }
       }
+      // lane gl now owns row r0 + j where j = bit-reversed (gl / (LPH/8)) pattern of the kept halves
+      int j = 0;
+      {
+        int half = 8, lanebit = LPH / 2;
+#pragma unroll
+        for (int step = 0; step < 3; ++step) {
+          half /= 2;
+          if (gl & lanebit) j += half;
+          lanebit >>= 1;
+        }
+      }
+      const int r = r0 + j;
+      const int h = g * PER_KV + y;
+      const bool owner = (gl < 8 * (LPH / 8)) && ((gl % (LPH / 8)) == 0);
+      if (owner && r < rows) {
+        if (r < rk) {
+          __nv_bfloat16 hi, lo;
+          split_bf16(acc[0], hi, lo);
+          const uint32_t off = (r >> 6) * NP * 128 + sw128_off(h, r & 63);
+          *reinterpret_cast<__nv_bfloat16*>(pimg + off) = hi;
+          *reinterpret_cast<__nv_bfloat16*>(pimg + plane + off) = lo;
+        } else {
+          tout[static_cast<long>(h) * p.s.tail_cap + (r - rk)] = acc[0];
+        }
+      }
+    }
     }
   }
 }
@@ -246,7 +315,7 @@ __global__ void __launch_bounds__(kStreamThreads) qdots_kernel(const FusedPlan p
 // ============================================================================
 template <int PER_KV, int D>
 __global__ void __launch_bounds__(kStreamThreads) vsum_kernel(const FusedPlan p, const FusedArgs a) {
-  constexpr int LPH = D / 8, RPI = 32 / LPH, NPART = 8 * RPI;
+  constexpr int LPH = D / 8, RPI = 32 / LPH, NPART = kStreamWarps * RPI;
   extern __shared__ __align__(16) float vsm[];
   const int g = blockIdx.x, b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -272,23 +341,22 @@ __global__ void __launch_bounds__(kStreamThreads) vsum_kernel(const FusedPlan p,
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[y][e] = 0.f;
   constexpr int U = 8;
-  const int stride = 8 * RPI;
+  const int stride = kStreamWarps * RPI;
   for (int r0 = warp * RPI + rsub; r0 < rows; r0 += U * stride) {
     uint4 raw[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int r = r0 + u * stride;
-      if (r < rows) raw[u] = ldg_stream(r < rv ? rvb + static_cast<long>(r) * W : tvb + static_cast<long>(r - rv) * W);
+    for (int u = 0; u < U; ++u) {  // clamped, unconditional loads: all stay in flight
+      const int r = min(r0 + u * stride, rows - 1);
+      raw[u] = ldg_stream(r < rv ? rvb + static_cast<long>(r) * W : tvb + static_cast<long>(r - rv) * W);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int r = r0 + u * stride;
-      if (r >= rows) break;
       float v[8];
       unpack8(raw[u], v);
 #pragma unroll
       for (int y = 0; y < PER_KV; ++y) {
-        const float w = wts[y * wstride + r];
+        const float w = r < rows ? wts[y * wstride + r] : 0.f;
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[y][e] = fmaf(w, v[e], acc[y][e]);
       }
@@ -320,9 +388,7 @@ __global__ void __launch_bounds__(kStreamThreads) vsum_kernel(const FusedPlan p,
 // ============================================================================
 template <int NPT>
 __global__ void __launch_bounds__(kThreads, 1)
-    core_kernel(const FusedPlan p, const __grid_constant__ CUtensorMap map_lk,
-                const __grid_constant__ CUtensorMap map_lv, const __grid_constant__ CUtensorMap map_lk32,
-                const __grid_constant__ CUtensorMap map_lv32, const FusedArgs a) {
+    core_kernel(const FusedPlan p, const FusedArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   const Smem L = smem_layout(p);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -339,11 +405,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int NS = p.stages;
 
   // ---- prologue: zero ring + P operand, barriers, TMEM -------------------------
-  {
-    uint4* z = reinterpret_cast<uint4*>(smem);
-    const uint32_t n16 = L.phi / 16;  // ring only (P arrives as a bulk copy)
-    for (uint32_t i = threadIdx.x; i < n16; i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
-  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
       mbar_init(&bars[kFull + s], 1);
@@ -364,10 +425,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ===================== producer: left_k / left_v panels =====================
     if (lane == 0) {
-      prefetch_tmap(&map_lk);
-      prefetch_tmap(&map_lv);
-      prefetch_tmap(&map_lk32);
-      prefetch_tmap(&map_lv32);
       {  // P operand image (bf16 hi/lo, already swizzled by qdots) -> smem in one bulk copy
         const uint32_t pbytes = 2u * p.kpk * NP * 128;
         mbar_expect_tx(&bars[kPopReady], pbytes);
@@ -393,16 +450,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         if (a.trace && i == it.lv0) a.trace[blockIdx.x * 16ull + 10] = global_ns();
-        const int row0 = tile * 128;
-        const int nbox = min(4, (it.chunk_len - row0 + 31) / 32);
-        mbar_expect_tx(full, static_cast<uint32_t>(nbox) * 4096u);
-        const int grow = b * p.s.n_comp + it.c_first + row0;
-        if (nbox == 4 && !p.box32_only) {  // full 128-token tile: one 16 KB box
-          tma_load_2d(dst, is_v ? &map_lv : &map_lk, panel * 64, grow, full);
-        } else {
-          for (int k = 0; k < nbox; ++k)
-            tma_load_2d(dst + k * 4096, is_v ? &map_lv32 : &map_lk32, panel * 64, grow + 32 * k, full);
-        }
+        // packed panel-major layout: one contiguous, pre-swizzled 16 KB block per (tile, panel)
+        const long gtile = static_cast<long>(a.inst0 + b) * p.ntiles + it.tile0 + tile;
+        const unsigned char* src = (is_v ? a.left_v_packed : a.left_k_packed) +
+                                   (gtile * (is_v ? p.vpanels_st : p.kpk) + panel) * static_cast<long>(kStageBytes);
+        mbar_expect_tx(full, kStageBytes);
+        bulk_load(dst, src, kStageBytes, full);
       }
     }
   } else if (warp == 1) {
@@ -427,7 +480,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bl = smem_desc(plo + kp * NP * 128 + kk * 32, 16, 1024, kSwizzle128B);
             const uint32_t d = tmem + static_cast<uint32_t>(t * NP);
             mma_bf16(d, ad, bh, idesc_s, (kp | kk) != 0);
-            mma_bf16(d, ad, bl, idesc_s, 1);
+            if (!(p.debug & 1)) mma_bf16(d, ad, bl, idesc_s, 1);
           }
           mma_commit(&bars[kEmpty + s]);
         }
@@ -457,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t bh = smem_desc(pth + boff, 16, 1024, kSwizzle128B);
             const uint64_t bl = smem_desc(ptl + boff, 16, 1024, kSwizzle128B);
             mma_bf16(d, ad, bh, idesc_u, (t | ks) != 0);
-            mma_bf16(d, ad, bl, idesc_u, 1);
+            if (!(p.debug & 1)) mma_bf16(d, ad, bl, idesc_u, 1);
           }
           mma_commit(&bars[kEmpty + s0]);
           mma_commit(&bars[kEmpty + s1]);
@@ -716,30 +769,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    KVP_CUDA(cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q));
-    require(q == cudaDriverEntryPointSuccess && p != nullptr, KVP_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-void encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t row_stride_bytes,
-               uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle sw) {
-  const cuuint64_t dims[2] = {cols, rows};
-  const cuuint64_t strides[1] = {row_stride_bytes};
-  const cuuint32_t box[2] = {box_cols, box_rows};
-  const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = tmap_encoder()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
-                                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  require(r == CUDA_SUCCESS, KVP_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-}
-
 }  // namespace
 
 FusedPlan plan_fused(const FusedShape& s) {
@@ -756,16 +785,15 @@ FusedPlan plan_fused(const FusedShape& s) {
   if (s.D != 128 && s.D != 64) return bad("fused path needs head_dim 64 or 128");
   if (s.H > 64) return bad("fused path supports up to 64 query heads");
   if (s.rank_k < 1 || s.rank_v < 1) return bad("fused path needs low-rank K and V");
-  if (s.ld_left % 8 != 0 || s.ld_left < std::max(s.rank_k, s.rank_v))
-    return bad("left-factor stride must be a multiple of 8 and cover both ranks");
   if (s.cluster < 1 || s.cluster > 8) return bad("cluster size must be 1..8");
   p.np = (s.H + 15) / 16 * 16;
   p.kpk = (s.rank_k + 63) / 64;
   p.vpanels = ((s.rank_v + 63) / 64 + 1) / 2 * 2;
   p.mtiles = p.vpanels / 2;
-  const int per = (s.n_comp + s.cluster - 1) / s.cluster;
-  p.chunk = (per + 31) / 32 * 32;
-  p.max_tiles = (p.chunk + 127) / 128;
+  p.ntiles = (s.n_comp + 127) / 128;
+  p.vpanels_st = (s.rank_v + 63) / 64;  // stored V panels (the even-pad panel is never stored)
+  p.max_tiles = (p.ntiles + s.cluster - 1) / s.cluster;
+  p.chunk = p.max_tiles * 128;
   p.tail_max = (s.tail_cap + s.cluster - 1) / s.cluster;
   if (p.tail_max > kTailMax) return bad("too many tail tokens per CTA (raise the cluster size)");
   p.heads_per_cta = (s.H + s.cluster - 1) / s.cluster;
@@ -785,8 +813,9 @@ FusedPlan plan_fused(const FusedShape& s) {
     if (want >= 2 && want <= kMaxStages && want % 2 == 0 && want < p.stages) p.stages = want;
   }
   p.box32_only = std::getenv("KVP_FUSED_BOX32") != nullptr;
+  if (const char* e = std::getenv("KVP_FUSED_DEBUG")) p.debug = std::atoi(e);  // timing experiments only
   p.smem_bytes = smem_layout(p).total;
-  const size_t vs = (static_cast<size_t>(per_kv) * ((s.rank_v + s.tail_cap + 3) & ~3) + 8 * (256 / s.D) * per_kv * s.D) * 4;
+  const size_t vs = (static_cast<size_t>(per_kv) * ((s.rank_v + s.tail_cap + 3) & ~3) + kStreamWarps * (256 / s.D) * per_kv * s.D) * 4;
   if (vs > 200 * 1024) return bad("vsum weights exceed shared memory");
   p.ok = true;
   p.why = "";
@@ -799,15 +828,6 @@ size_t fused_workspace_bytes(const FusedShape& s) {
   return static_cast<size_t>(s.batch) * (pimg + sizeof(float) * s.H * (static_cast<size_t>(s.tail_cap) + s.rank_v));
 }
 
-void encode_fused_maps(const FusedShape& s, const void* left_k, const void* left_v, CUtensorMap* maps) {
-  const uint64_t rows = static_cast<uint64_t>(s.batch) * s.n_comp;
-  const uint64_t ld = static_cast<uint64_t>(s.ld_left) * 2;
-  encode_2d(&maps[0], left_k, s.rank_k, rows, ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-  encode_2d(&maps[1], left_v, s.rank_v, rows, ld, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-  encode_2d(&maps[2], left_k, s.rank_k, rows, ld, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-  encode_2d(&maps[3], left_v, s.rank_v, rows, ld, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-}
-
 template <int PER_KV, int D>
 void launch_stream_pair(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, bool first) {
   const dim3 grid(static_cast<unsigned>(p.s.Hkv), static_cast<unsigned>(p.s.batch));
@@ -815,7 +835,7 @@ void launch_stream_pair(const FusedPlan& p, const FusedArgs& a, cudaStream_t st,
     qdots_kernel<PER_KV, D><<<grid, kStreamThreads, 0, st>>>(p, a);
     KVP_LAUNCHED();
   } else {
-    const size_t smem = (static_cast<size_t>(PER_KV) * ((p.s.rank_v + p.s.tail_cap + 3) & ~3) + 8 * (256 / D) * PER_KV * D) * 4;
+    const size_t smem = (static_cast<size_t>(PER_KV) * ((p.s.rank_v + p.s.tail_cap + 3) & ~3) + kStreamWarps * (256 / D) * PER_KV * D) * 4;
     static size_t attr = 0;
     if (attr < smem) {
       KVP_CUDA(cudaFuncSetAttribute(vsum_kernel<PER_KV, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -840,8 +860,7 @@ void launch_stream(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, bool
   }
 }
 
-using CoreFn = void (*)(const FusedPlan, const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap,
-                       const __grid_constant__ CUtensorMap, const __grid_constant__ CUtensorMap, const FusedArgs);
+using CoreFn = void (*)(const FusedPlan, const FusedArgs);
 CoreFn core_for(int np) {
   switch (np) {
     case 16: return core_kernel<16>;
@@ -851,9 +870,10 @@ CoreFn core_for(int np) {
   }
 }
 
-void launch_fused(const FusedPlan& p, const CUtensorMap* maps, const FusedArgs& a, cudaStream_t st) {
-  require(p.ok, KVP_ERR_PARAMETER, p.why);
-  launch_stream(p, a, st, true);
+void launch_qdots(const FusedPlan& p, const FusedArgs& a, cudaStream_t st) { launch_stream(p, a, st, true); }
+void launch_vsum(const FusedPlan& p, const FusedArgs& a, cudaStream_t st) { launch_stream(p, a, st, false); }
+
+void launch_core(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, int priority) {
   auto kernel = core_for(p.np);
   KVP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_bytes)));
   cudaLaunchConfig_t cfg{};
@@ -861,16 +881,43 @@ void launch_fused(const FusedPlan& p, const CUtensorMap* maps, const FusedArgs& 
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = p.smem_bytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(p.s.cluster);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = priority;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  KVP_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, maps[0], maps[1], maps[2], maps[3], a));
+  cfg.numAttrs = priority != 0 ? 2 : 1;
+  KVP_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, a));
   KVP_LAUNCHED();
-  launch_stream(p, a, st, false);
+}
+
+void launch_fused(const FusedPlan& p, const FusedArgs& a, cudaStream_t st) {
+  require(p.ok, KVP_ERR_PARAMETER, p.why);
+  launch_qdots(p, a, st);
+  launch_core(p, a, st, 0);
+  launch_vsum(p, a, st);
+}
+
+FusedArgs offset_args(const FusedPlan& full, const FusedArgs& a, int b0) {
+  FusedArgs o = a;
+  const long W = static_cast<long>(full.s.Hkv) * full.s.D, H = full.s.H;
+  o.right_k += b0 * full.s.rank_k * W;
+  o.right_v += b0 * full.s.rank_v * W;
+  o.tail_k += b0 * full.s.tail_cap * W;
+  o.tail_v += b0 * full.s.tail_cap * W;
+  o.q += b0 * a.q_stride;
+  if (o.importance) o.importance += b0 * a.imp_stride;
+  if (o.head_avg) o.head_avg += static_cast<long>(b0) * (full.s.n_comp + full.s.tail_cap);
+  const long ctx_elem = H * full.s.D;
+  o.ctx_out = static_cast<char*>(a.ctx_out) + b0 * ctx_elem * (a.ctx_bf16 ? 2 : 4);
+  o.ws_pimg += static_cast<size_t>(b0) * 2 * full.kpk * full.np * 128;
+  o.ws_tail += b0 * H * full.s.tail_cap;
+  o.ws_u += b0 * H * full.s.rank_v;
+  o.inst0 = a.inst0 + b0;
+  return o;
 }
 
 int max_active_clusters(const FusedPlan& p) {
@@ -894,22 +941,90 @@ int max_active_clusters(const FusedPlan& p) {
 
 }  // namespace kvp
 
+namespace kvp {
+namespace {
+// Row-major left factor [n][ld] (bf16) -> packed panel-major, pre-swizzled tiles.
+__global__ void pack_left_kernel(const __nv_bfloat16* src, long ld, int n, int rank, int ntiles, int panels,
+                                 unsigned char* dst) {
+  const long total = static_cast<long>(ntiles) * panels * 128 * 64;  // elements per instance
+  const int b = blockIdx.y;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i % 64), row = static_cast<int>((i / 64) % 128);
+    const long blk = i / (64 * 128);
+    const int panel = static_cast<int>(blk % panels), tile = static_cast<int>(blk / panels);
+    const int t = tile * 128 + row, r = panel * 64 + k;
+    const __nv_bfloat16 v = (t < n && r < rank) ? src[(static_cast<long>(b) * n + t) * ld + r] : __float2bfloat16_rn(0.f);
+    unsigned char* out = dst + (static_cast<long>(b) * ntiles * panels + blk) * static_cast<long>(kStageBytes);
+    *reinterpret_cast<__nv_bfloat16*>(out + sm100::sw128_off(row, k)) = v;
+  }
+}
+}  // namespace
+
+size_t packed_left_bytes(int batch, int n, int rank) {
+  return static_cast<size_t>(batch) * ((n + 127) / 128) * ((rank + 63) / 64) * kStageBytes;
+}
+
+void pack_left(const void* src, long ld, int batch, int n, int rank, void* dst, cudaStream_t st) {
+  const int ntiles = (n + 127) / 128, panels = (rank + 63) / 64;
+  pack_left_kernel<<<dim3(64, batch), 256, 0, st>>>(static_cast<const __nv_bfloat16*>(src), ld, n, rank, ntiles, panels,
+                                                     static_cast<unsigned char*>(dst));
+  KVP_LAUNCHED();
+}
+}  // namespace kvp
+
+extern "C" size_t kvp_packed_left_bytes(int32_t batch, int32_t n, int32_t rank) {
+  return kvp::packed_left_bytes(batch, n, rank);
+}
+
+extern "C" int kvp_pack_left(const void* src, int64_t ld, int32_t batch, int32_t n, int32_t rank, void* dst,
+                             void* stream) {
+  return kvp::guarded([&] {
+    kvp::require(src && dst && batch > 0 && n > 0 && rank > 0 && ld >= rank, KVP_ERR_PARAMETER,
+                 "pack_left: bad arguments");
+    kvp::pack_left(src, ld, batch, n, rank, dst, kvp::as_stream(stream));
+  });
+}
+
 // Debug hooks (not part of the public header).
 static unsigned long long* g_trace = nullptr;
 extern "C" void kvp_debug_fused_trace(void* dev_buffer) { g_trace = static_cast<unsigned long long*>(dev_buffer); }
 
 namespace {
-// Cluster size: 4 CTAs per instance when the plan fits (measured fastest on
-// B200 for the C2/C5 shapes), else 8, 2, 1.
+// Cluster size (CTAs per instance): minimise waves x tiles-per-CTA, where
+// waves = ceil(batch / co-resident clusters of that size).  Measured on B200
+// for the C2 shape: 6 (1 wave x 3 tiles) beats 4, 5, 7 and 8.
 int auto_cluster(kvp::FusedShape s) {
-  for (int c : {4, 8, 2, 1}) {
+  static std::map<std::tuple<int, int, int, int, int, int, int, int>, int> cache;
+  const auto key = std::make_tuple(s.H, s.Hkv, s.D, s.n_comp, s.rank_k, s.rank_v, s.tail_cap, s.batch);
+  if (auto it = cache.find(key); it != cache.end()) return it->second;
+  int best = 0;
+  long best_cost = 1L << 40;
+  for (int c = 8; c >= 1; --c) {
     s.cluster = c;
-    if (kvp::plan_fused(s).ok) return c;
+    const kvp::FusedPlan p = kvp::plan_fused(s);
+    if (!p.ok) continue;
+    int active = 1;
+    try {
+      active = std::max(1, kvp::max_active_clusters(p));
+    } catch (...) {
+      active = 148 / c;
+    }
+    const long waves = (s.batch + active - 1) / active;
+    const long cost = waves * p.max_tiles;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = c;
+    }
   }
-  return 8;
+  cache[key] = best > 0 ? best : 8;
+  return cache[key];
 }
+}  // namespace
+int kvp::auto_cluster_size(const kvp::FusedShape& s) { return auto_cluster(s); }
+namespace {
 kvp::FusedShape shape_of(const kvp_fused_desc* d) {
-  kvp::FusedShape s{d->heads, d->kv_heads, d->head_dim, d->n_comp, d->rank_k, d->rank_v, d->ld_left,
+  kvp::FusedShape s{d->heads, d->kv_heads, d->head_dim, d->n_comp, d->rank_k, d->rank_v, 0,
                     d->tail_cap, d->batch, d->cluster};
   if (s.cluster <= 0) s.cluster = auto_cluster(s);
   return s;
@@ -949,9 +1064,9 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     } else {
       require(d->workspace_bytes >= ws_bytes, KVP_ERR_PARAMETER, "decode_fused: workspace too small");
     }
-    CUtensorMap maps[4];
-    encode_fused_maps(s, d->left_k, d->left_v, maps);
     FusedArgs a{};
+    a.left_k_packed = static_cast<const unsigned char*>(d->left_k);
+    a.left_v_packed = static_cast<const unsigned char*>(d->left_v);
     a.right_k = static_cast<const __nv_bfloat16*>(d->right_k);
     a.right_v = static_cast<const __nv_bfloat16*>(d->right_v);
     a.tail_k = static_cast<const __nv_bfloat16*>(d->tail_k);
@@ -959,6 +1074,9 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     a.n_tail_dev = d->n_tail_dev;
     a.n_tail = d->n_tail;
     a.q = d->queries;
+    a.q_stride = static_cast<long>(s.H) * s.D;
+    a.append_kv = 0;
+    a.inst0 = 0;
     a.importance = d->importance;
     a.imp_stride = d->imp_stride;
     const double decay = std::pow(d->alpha, 1.0);  // alpha^T_q, importance.cpp:58
@@ -971,6 +1089,6 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     a.ws_tail = reinterpret_cast<float*>(a.ws_pimg + static_cast<size_t>(s.batch) * 2 * p.kpk * p.np * 128);
     a.ws_u = a.ws_tail + static_cast<size_t>(s.batch) * s.H * s.tail_cap;
     a.trace = g_trace;
-    launch_fused(p, maps, a, st);
+    launch_fused(p, a, st);
   });
 }

@@ -15,20 +15,29 @@ struct FusedShape {
   int H, Hkv, D;      // geometry
   int n_comp;         // compressed (visual) tokens per instance
   int rank_k, rank_v; // stored ranks
-  int ld_left;        // row stride of left factors (elements, multiple of 8)
+  int ld_left;        // unused (left factors are packed)
   int tail_cap;       // tail rows allocated per instance
   int batch;
   int cluster;        // CTAs per instance in the low-rank core kernel
 };
 
 struct FusedArgs {
+  // left factors in the packed layout (pack_left): per instance, per 128-token
+  // tile, per 64-rank panel one contiguous 16 KB block, rows 128 B, 16 B chunks
+  // XOR-swizzled by row % 8 (the tcgen05 SWIZZLE_128B K-major operand layout)
+  const unsigned char* left_k_packed;  // [batch][ntiles][kpk][16 KB]
+  const unsigned char* left_v_packed;  // [batch][ntiles][vpanels_st][16 KB]
   const __nv_bfloat16* right_k;  // [batch][rank_k][W]
   const __nv_bfloat16* right_v;  // [batch][rank_v][W]
   const __nv_bfloat16* tail_k;   // [batch][tail_cap][W]
   const __nv_bfloat16* tail_v;
   const int* n_tail_dev;         // device counter of valid tail rows (nullable)
   int n_tail;                    // used when n_tail_dev == nullptr
-  const float* q;                // [batch][H*D], raw (unscaled) queries
+  const float* q;                // [batch][q_stride] raw (unscaled) queries (first H*D of each row)
+  long q_stride;                 // row stride of q (H*D, or H*D + 2W when q points into [q|k|v])
+  int append_kv;                 // 1: q rows are [q|k|v]; qdots appends k, v as tail row n_tail-1 and
+                                 //    zeroes that token's importance (cache.cpp:147-170)
+  int inst0;                     // first instance of this launch inside the tensor-mapped left factors
   double* importance;            // [batch][imp_stride]: compressed then tail (nullable)
   long imp_stride;
   double ema_decay, ema_blend;   // alpha^1, 1 - alpha^1 (T_q = 1)
@@ -49,12 +58,15 @@ struct FusedPlan {
   int kpk;             // K panels of rank_k (64 ranks each)
   int vpanels;         // V panels, even
   int mtiles;          // vpanels / 2
-  int chunk;           // compressed tokens per CTA (multiple of 32)
-  int max_tiles;       // ceil(chunk / 128)
+  int ntiles;          // 128-token tiles per instance
+  int vpanels_st;      // stored V panels (ceil(rank_v / 64))
+  int chunk;           // compressed tokens per CTA (max_tiles * 128)
+  int max_tiles;       // tiles per CTA
   int tail_max;        // max tail tokens per CTA
   int heads_per_cta;   // query heads per CTA in the U reduce-scatter
   int stages;          // TMA ring stages (even)
   bool box32_only;     // tuning: force 32-row TMA boxes
+  int debug;           // timing experiments (1: skip the lo-half MMAs — wrong numerics)
   size_t smem_bytes;
   int tmem_cols;
   bool ok;
@@ -62,8 +74,16 @@ struct FusedPlan {
 };
 
 FusedPlan plan_fused(const FusedShape& s);
+int auto_cluster_size(const FusedShape& s);  // occupancy-aware CTAs per instance
 size_t fused_workspace_bytes(const FusedShape& s);
-void encode_fused_maps(const FusedShape& s, const void* left_k, const void* left_v, CUtensorMap* maps /*[4]*/);
-void launch_fused(const FusedPlan& p, const CUtensorMap* maps, const FusedArgs& a, cudaStream_t st);
+size_t packed_left_bytes(int batch, int n, int rank);
+void pack_left(const void* src, long ld, int batch, int n, int rank, void* dst, cudaStream_t st);
+void launch_fused(const FusedPlan& p, const FusedArgs& a, cudaStream_t st);
+// The three launches separately (engine pipelining across instance groups).
+void launch_qdots(const FusedPlan& p, const FusedArgs& a, cudaStream_t st);
+void launch_core(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, int priority);
+void launch_vsum(const FusedPlan& p, const FusedArgs& a, cudaStream_t st);
+// Offsets every per-instance pointer of `a` by `b0` instances (workspace included).
+FusedArgs offset_args(const FusedPlan& full, const FusedArgs& a, int b0);
 
 }  // namespace kvp

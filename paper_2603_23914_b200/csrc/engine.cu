@@ -15,6 +15,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -34,15 +35,20 @@ struct kvp_engine {
   void* blas_ws = nullptr;
   // buffers
   __nv_bfloat16 *wqkv = nullptr, *wo = nullptr;
-  __nv_bfloat16 *lk = nullptr, *lv = nullptr, *rkf = nullptr, *rvf = nullptr, *tk = nullptr, *tv = nullptr;
+  unsigned char *lk = nullptr, *lv = nullptr;  // packed left factors [L][...]
+  __nv_bfloat16 *rkf = nullptr, *rvf = nullptr, *tk = nullptr, *tv = nullptr;
   double* imp = nullptr;
   __nv_bfloat16 *xb = nullptr, *ctx = nullptr;
   float *qkv = nullptr, *q = nullptr, *xin = nullptr, *xcur = nullptr, *yout = nullptr;
   int* n_tail_dev = nullptr;
   void* fused_ws = nullptr;
   size_t fused_ws_bytes = 0;
-  kvp::FusedPlan plan{};
-  std::vector<CUtensorMap> maps;  // [L][4]
+  kvp::FusedPlan plan{};   // whole batch (workspace, tensor maps)
+  kvp::FusedPlan gplan{};  // one instance group (launch grids)
+  int groups = 1;          // instance groups pipelined across two streams
+  int core_priority = 0;
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_q0 = nullptr, ev_join = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   double compaction_ms = 0.0;
@@ -62,9 +68,13 @@ struct kvp_engine {
     if (graph) cudaGraphDestroy(graph);
     for (void* p : allocations) cudaFree(p);
     if (blas) cublasDestroy(blas);
+    for (cudaEvent_t ev : {ev_fork, ev_q0, ev_join})
+      if (ev) cudaEventDestroy(ev);
+    if (stream2) cudaStreamDestroy(stream2);
     if (stream) cudaStreamDestroy(stream);
   }
-  size_t left_elems() const { return static_cast<size_t>(B) * n * ld; }
+  size_t lk_bytes() const { return kvp::packed_left_bytes(B, n, rk); }  // per layer, packed
+  size_t lv_bytes() const { return kvp::packed_left_bytes(B, n, rv); }
   size_t right_k_elems() const { return static_cast<size_t>(B) * rk * W; }
   size_t right_v_elems() const { return static_cast<size_t>(B) * rv * W; }
   size_t tail_elems() const { return static_cast<size_t>(B) * cap * W; }
@@ -115,15 +125,15 @@ __global__ void latent_direct_kernel(__nv_bfloat16* out, long ld_out, int T, int
 }
 
 // Placeholder factors for factor_init = 1 (decode-only benchmarking): left
-// rows N(0,1) * 0.98^r, right rows N(0,1)/sqrt(W) (near-orthonormal for W >> R).
-__global__ void synth_factor_kernel(__nv_bfloat16* left, int n, int ld, int rank, __nv_bfloat16* right, int W,
-                                    uint64_t seed, uint64_t stream) {
+// rows N(0,1) * 0.98^r (row-major scratch, packed afterwards), right rows
+// N(0,1)/sqrt(W) (near-orthonormal for W >> R).
+__global__ void synth_factor_kernel(__nv_bfloat16* left, int n, int rank, __nv_bfloat16* right, int W, uint64_t seed,
+                                    uint64_t stream) {
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const long nl = static_cast<long>(n) * ld, nr = static_cast<long>(rank) * W;
+  const long nl = static_cast<long>(n) * rank, nr = static_cast<long>(rank) * W;
   if (i < nl) {
-    const int r = static_cast<int>(i % ld);
-    const float v = r < rank ? static_cast<float>(philox_gaussian(seed, stream, i) * pow(0.98, r)) : 0.f;
-    left[i] = __float2bfloat16_rn(v);
+    const int r = static_cast<int>(i % rank);
+    left[i] = __float2bfloat16_rn(static_cast<float>(philox_gaussian(seed, stream, i) * pow(0.98, r)));
   } else if (i < nl + nr) {
     const long k = i - nl;
     right[k] = __float2bfloat16_rn(static_cast<float>(philox_gaussian(seed, stream ^ 0x5A5Aull, k)) * rsqrtf(float(W)));
@@ -163,25 +173,31 @@ void launch_1d(long n, auto&& f) {
   KVP_LAUNCHED();
 }
 
-// Row-major C (m x n, fp32) = A (m x k, bf16) * B (k x n, bf16), ldb = n_total.
-void gemm_bf16(kvp_engine* e, int m, int n, int k, const __nv_bfloat16* a, const __nv_bfloat16* b, int ldb,
-               float* c) {
+// Row-major C (m x n) = A (m x k, bf16) * B (k x n, bf16), fp32 accumulate;
+// C is fp32 or bf16 (the next layer's input needs no separate cast).
+void gemm_bf16(kvp_engine* e, int m, int n, int k, const __nv_bfloat16* a, const __nv_bfloat16* b, int ldb, void* c,
+               bool c_bf16) {
   const float one = 1.f, zero = 0.f;
   blas_check(cublasGemmEx(e->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, m, k, &one, b, CUDA_R_16BF, ldb, a, CUDA_R_16BF, k,
-                          &zero, c, CUDA_R_32F, n, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
+                          &zero, c, c_bf16 ? CUDA_R_16BF : CUDA_R_32F, n, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
              "cublasGemmEx");
 }
 
 FusedArgs fused_args(kvp_engine* e, int l) {
   FusedArgs a{};
   const size_t lidx = static_cast<size_t>(l);
+  a.left_k_packed = e->lk + lidx * e->lk_bytes();
+  a.left_v_packed = e->lv + lidx * e->lv_bytes();
   a.right_k = e->rkf + lidx * e->right_k_elems();
   a.right_v = e->rvf + lidx * e->right_v_elems();
   a.tail_k = e->tk + lidx * e->tail_elems();
   a.tail_v = e->tv + lidx * e->tail_elems();
   a.n_tail_dev = e->n_tail_dev;
   a.n_tail = 0;
-  a.q = e->q;
+  a.q = e->qkv;  // [q | k | v] rows straight from the projection GEMM
+  a.q_stride = static_cast<long>(e->HD) + 2L * e->W;
+  a.append_kv = 1;  // qdots appends k, v to the tail and zeroes the new importance
+  a.inst0 = 0;
   a.importance = e->imp + lidx * e->B * e->imp_stride();
   a.imp_stride = static_cast<long>(e->imp_stride());
   a.ema_decay = std::pow(e->cfg.alpha, 1.0);
@@ -196,26 +212,51 @@ FusedArgs fused_args(kvp_engine* e, int l) {
   return a;
 }
 
+// Attention for one layer, instance groups pipelined over two streams:
+// qdots(g0) -> [core(g0) || qdots(g1)] -> [vsum(g0) || core(g1)] -> vsum(g1).
+void enqueue_attention(kvp_engine* e, int l) {
+  cudaStream_t s = e->stream;
+  const FusedArgs full = fused_args(e, l);
+  if (e->groups == 1) {
+    launch_qdots(e->gplan, full, s);
+    launch_core(e->gplan, full, s, e->core_priority);
+    launch_vsum(e->gplan, full, s);
+    return;
+  }
+  const int gb = e->gplan.s.batch;
+  KVP_CUDA(cudaEventRecord(e->ev_fork, s));
+  KVP_CUDA(cudaStreamWaitEvent(e->stream2, e->ev_fork, 0));
+  const FusedArgs a0 = offset_args(e->plan, full, 0);
+  launch_qdots(e->gplan, a0, s);
+  KVP_CUDA(cudaEventRecord(e->ev_q0, s));
+  launch_core(e->gplan, a0, s, e->core_priority);
+  launch_vsum(e->gplan, a0, s);
+  for (int g = 1; g < e->groups; ++g) {
+    const FusedArgs ag = offset_args(e->plan, full, g * gb);
+    KVP_CUDA(cudaStreamWaitEvent(e->stream2, e->ev_q0, 0));
+    launch_qdots(e->gplan, ag, e->stream2);
+    KVP_CUDA(cudaEventRecord(e->ev_q0, e->stream2));
+    launch_core(e->gplan, ag, e->stream2, e->core_priority);
+    launch_vsum(e->gplan, ag, e->stream2);
+  }
+  KVP_CUDA(cudaEventRecord(e->ev_join, e->stream2));
+  KVP_CUDA(cudaStreamWaitEvent(s, e->ev_join, 0));
+}
+
 // One decode step over all layers, enqueued on e->stream (graph-capturable).
 void enqueue_step(kvp_engine* e) {
   cudaStream_t s = e->stream;
   bump_counter_kernel<<<1, 1, 0, s>>>(e->n_tail_dev);
   KVP_LAUNCHED();
   const long nx = static_cast<long>(e->B) * e->HD;
-  const float* x = e->xin;
+  launch_1d(nx, [&](unsigned g, int t) { to_bf16_kernel<<<g, t, 0, s>>>(e->xin, e->xb, nx); });
+  const int nqkv = e->HD + 2 * e->W;
   for (int l = 0; l < e->L; ++l) {
-    launch_1d(nx, [&](unsigned g, int t) { to_bf16_kernel<<<g, t, 0, s>>>(x, e->xb, nx); });
-    const int nqkv = e->HD + 2 * e->W;
-    gemm_bf16(e, e->B, nqkv, e->HD, e->xb, e->wqkv + static_cast<size_t>(l) * e->HD * nqkv, nqkv, e->qkv);
-    append_kernel<<<dim3(16, e->B), 256, 0, s>>>(e->qkv, e->q, e->tk + static_cast<size_t>(l) * e->tail_elems(),
-                                                  e->tv + static_cast<size_t>(l) * e->tail_elems(),
-                                                  e->imp + static_cast<size_t>(l) * e->B * e->imp_stride(), e->n_tail_dev,
-                                                  e->HD, e->W, e->cap, e->n, static_cast<long>(e->imp_stride()));
-    KVP_LAUNCHED();
-    launch_fused(e->plan, &e->maps[static_cast<size_t>(l) * 4], fused_args(e, l), s);
-    float* out = (l + 1 == e->L) ? e->yout : e->xcur;
-    gemm_bf16(e, e->B, e->HD, e->HD, e->ctx, e->wo + static_cast<size_t>(l) * e->HD * e->HD, e->HD, out);
-    x = out;
+    gemm_bf16(e, e->B, nqkv, e->HD, e->xb, e->wqkv + static_cast<size_t>(l) * e->HD * nqkv, nqkv, e->qkv, false);
+    enqueue_attention(e, l);
+    const bool last = l + 1 == e->L;
+    gemm_bf16(e, e->B, e->HD, e->HD, e->ctx, e->wo + static_cast<size_t>(l) * e->HD * e->HD, e->HD,
+              last ? static_cast<void*>(e->yout) : static_cast<void*>(e->xb), !last);
   }
 }
 
@@ -266,17 +307,25 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     e->cap = c->textual_tokens + c->decode_steps;
     e->rk = std::min(c->rank_k, std::min(e->n, e->W));  // compress_segment clamp (compressor.cpp:46-59)
     e->rv = std::min(c->rank_v, std::min(e->n, e->W));
-    e->ld = (std::max(e->rk, e->rv) + 63) / 64 * 64;
+    e->ld = 0;
     FusedShape fs{e->H, e->Hkv, e->D, e->n, e->rk, e->rv, e->ld, e->cap, e->B, c->cluster};
-    if (fs.cluster <= 0) {
-      for (int cl : {4, 8, 2, 1}) {
-        fs.cluster = cl;
-        if (plan_fused(fs).ok) break;
-      }
-    }
+    if (fs.cluster <= 0) fs.cluster = auto_cluster_size(fs);
     e->plan = plan_fused(fs);
     require(e->plan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->plan.why).c_str());
+    e->groups = 1;  // two-group pipelining measured slower on B200 (KVP_GROUPS to override)
+    if (const char* g = std::getenv("KVP_GROUPS")) e->groups = std::max(1, std::atoi(g));
+    require(e->B % e->groups == 0, KVP_ERR_PARAMETER, "engine: batch must divide into the instance groups");
+    FusedShape gs = fs;
+    gs.batch = e->B / e->groups;
+    e->gplan = plan_fused(gs);
+    require(e->gplan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->gplan.why).c_str());
+    int lo = 0, hi = 0;
+    KVP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    e->core_priority = hi;  // numerically lowest = highest priority
     KVP_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    KVP_CUDA(cudaStreamCreateWithFlags(&e->stream2, cudaStreamNonBlocking));
+    for (cudaEvent_t* ev : {&e->ev_fork, &e->ev_q0, &e->ev_join})
+      KVP_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     blas_check(cublasCreate(&e->blas), "cublasCreate");
     blas_check(cublasSetStream(e->blas, e->stream), "cublasSetStream");
     const size_t blas_ws = 32u << 20;
@@ -285,8 +334,8 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     const size_t L = e->L;
     e->wqkv = e->alloc<__nv_bfloat16>(L * e->HD * (e->HD + 2 * e->W));
     e->wo = e->alloc<__nv_bfloat16>(L * e->HD * e->HD);
-    e->lk = e->alloc<__nv_bfloat16>(L * e->left_elems());
-    e->lv = e->alloc<__nv_bfloat16>(L * e->left_elems());
+    e->lk = e->alloc<unsigned char>(L * e->lk_bytes());
+    e->lv = e->alloc<unsigned char>(L * e->lv_bytes());
     e->rkf = e->alloc<__nv_bfloat16>(L * e->right_k_elems());
     e->rvf = e->alloc<__nv_bfloat16>(L * e->right_v_elems());
     e->tk = e->alloc<__nv_bfloat16>(L * e->tail_elems());
@@ -303,9 +352,6 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     e->fused_ws_bytes = fused_workspace_bytes(fs);
     e->fused_ws = e->alloc<char>(e->fused_ws_bytes);
     KVP_CUDA(cudaMemset(e->fused_ws, 0, e->fused_ws_bytes));
-    e->maps.resize(L * 4);
-    for (size_t l = 0; l < L; ++l)
-      encode_fused_maps(fs, e->lk + l * e->left_elems(), e->lv + l * e->left_elems(), &e->maps[l * 4]);
     *out = e.release();
   });
 }
@@ -357,19 +403,25 @@ extern "C" int kvp_engine_prefill(kvp_engine* e) {
     KVP_CUDA(cudaEventCreate(&e1));
     KVP_CUDA(cudaEventRecord(e0, s));
     if (e->cfg.factor_init == 1) {
+      __nv_bfloat16* scratch = nullptr;
+      KVP_CUDA(cudaMallocAsync(&scratch, sizeof(__nv_bfloat16) * e->B * e->n * std::max(e->rk, e->rv), s));
       for (int l = 0; l < e->L; ++l)
-        for (int b = 0; b < e->B; ++b)
-          for (int kind = 0; kind < 2; ++kind) {
-            const int rank = kind == 0 ? e->rk : e->rv;
-            __nv_bfloat16* left = (kind == 0 ? e->lk : e->lv) + static_cast<size_t>(l) * e->left_elems() +
-                                  static_cast<size_t>(b) * e->n * e->ld;
+        for (int kind = 0; kind < 2; ++kind) {
+          const int rank = kind == 0 ? e->rk : e->rv;
+          for (int b = 0; b < e->B; ++b) {
             __nv_bfloat16* right = (kind == 0 ? e->rkf + static_cast<size_t>(l) * e->right_k_elems()
                                               : e->rvf + static_cast<size_t>(l) * e->right_v_elems()) +
                                    static_cast<size_t>(b) * rank * e->W;
-            launch_1d(static_cast<long>(e->n) * e->ld + static_cast<long>(rank) * e->W, [&](unsigned g, int t) {
-              synth_factor_kernel<<<g, t, 0, s>>>(left, e->n, e->ld, rank, right, e->W, seed, stream_id(2, b, l, kind));
+            launch_1d(static_cast<long>(e->n) * rank + static_cast<long>(rank) * e->W, [&](unsigned g, int t) {
+              synth_factor_kernel<<<g, t, 0, s>>>(scratch + static_cast<size_t>(b) * e->n * rank, e->n, rank, right,
+                                                  e->W, seed, stream_id(2, b, l, kind));
             });
           }
+          unsigned char* dst = kind == 0 ? e->lk + static_cast<size_t>(l) * e->lk_bytes()
+                                         : e->lv + static_cast<size_t>(l) * e->lv_bytes();
+          pack_left(scratch, rank, e->B, e->n, rank, dst, s);
+        }
+      KVP_CUDA(cudaFreeAsync(scratch, s));
     } else {
       compact_visual(e);
     }
@@ -462,8 +514,8 @@ extern "C" int kvp_engine_layer_state(kvp_engine* e, int layer, kvp_engine_layer
     require(e && v, KVP_ERR_PARAMETER, "engine: null argument");
     require(layer >= 0 && layer < e->L, KVP_ERR_PARAMETER, "engine: layer out of range");
     const size_t l = layer;
-    v->left_k = e->lk + l * e->left_elems();
-    v->left_v = e->lv + l * e->left_elems();
+    v->left_k = e->lk + l * e->lk_bytes();
+    v->left_v = e->lv + l * e->lv_bytes();
     v->right_k = e->rkf + l * e->right_k_elems();
     v->right_v = e->rvf + l * e->right_v_elems();
     v->tail_k = e->tk + l * e->tail_elems();
@@ -488,7 +540,7 @@ extern "C" int kvp_engine_time_attention(kvp_engine* e, int32_t iters, double* m
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;
     KVP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    for (int l = 0; l < e->L; ++l) launch_fused(e->plan, &e->maps[static_cast<size_t>(l) * 4], fused_args(e, l), s);
+    for (int l = 0; l < e->L; ++l) enqueue_attention(e, l);
     KVP_CUDA(cudaStreamEndCapture(s, &g));
     KVP_CUDA(cudaGraphInstantiate(&ge, g, 0));
     KVP_CUDA(cudaGraphLaunch(ge, s));  // warm-up

@@ -19,16 +19,7 @@ def _torch():
     return torch
 
 
-class FusedDesc(C.Structure):
-    _fields_ = [("heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("batch", C.c_int32),
-                ("n_comp", C.c_int32), ("rank_k", C.c_int32), ("rank_v", C.c_int32), ("ld_left", C.c_int32),
-                ("tail_cap", C.c_int32), ("n_tail", C.c_int32), ("n_tail_dev", C.c_void_p),
-                ("cluster", C.c_int32), ("context_bf16", C.c_int32),
-                ("left_k", C.c_void_p), ("right_k", C.c_void_p), ("left_v", C.c_void_p), ("right_v", C.c_void_p),
-                ("tail_k", C.c_void_p), ("tail_v", C.c_void_p), ("queries", C.c_void_p),
-                ("importance", C.c_void_p), ("imp_stride", C.c_int64), ("alpha", C.c_double),
-                ("head_avg", C.c_void_p), ("context", C.c_void_p), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_size_t)]
+from paper_2603_23914_b200._capi import FusedDesc  # noqa: E402
 
 
 def bf16_round(x):
@@ -81,18 +72,19 @@ def run_fused(case, H, Hkv, D, nt, alpha, cluster=0, ld_pad=8):
     B, n, rk = case["left_k"].shape
     rv = case["left_v"].shape[2]
     cap = case["tail_k"].shape[1]
-    ld = ((max(rk, rv) + ld_pad - 1) // ld_pad) * ld_pad
-    def left(x):
-        out = torch.zeros((B, n, ld), dtype=torch.bfloat16)
-        out[:, :, :x.shape[2]] = torch.as_tensor(x)
-        return out.cuda()
+    def left(x):  # row-major bf16 -> packed panel-major layout (kvp_pack_left)
+        src = torch.as_tensor(x).to(torch.bfloat16).cuda().contiguous()
+        r = x.shape[2]
+        out = torch.zeros(capi.lib().kvp_packed_left_bytes(B, n, r), dtype=torch.uint8, device="cuda")
+        capi.call("kvp_pack_left", src.data_ptr(), r, B, n, r, out.data_ptr(), None)
+        return out
     bf = lambda x: torch.as_tensor(x).to(torch.bfloat16).cuda().contiguous()
     t = dict(lk=left(case["left_k"]), lv=left(case["left_v"]), rk=bf(case["right_k"]), rv=bf(case["right_v"]),
              tk=bf(case["tail_k"]), tv=bf(case["tail_v"]), q=torch.as_tensor(case["q"], dtype=torch.float32).cuda(),
              imp=torch.as_tensor(case["imp"]).cuda().contiguous())
     ctx = torch.zeros((B, H * D), dtype=torch.float32, device="cuda")
     ha = torch.zeros((B, n + cap), dtype=torch.float32, device="cuda")
-    d = FusedDesc(H, Hkv, D, B, n, rk, rv, ld, cap, nt, None, cluster, 0, t["lk"].data_ptr(), t["rk"].data_ptr(),
+    d = FusedDesc(H, Hkv, D, B, n, rk, rv, 0, cap, nt, None, cluster, 0, t["lk"].data_ptr(), t["rk"].data_ptr(),
                   t["lv"].data_ptr(), t["rv"].data_ptr(), t["tk"].data_ptr(), t["tv"].data_ptr(), t["q"].data_ptr(),
                   t["imp"].data_ptr(), n + cap, alpha, ha.data_ptr(), ctx.data_ptr())
     capi.lib().kvp_decode_fused.argtypes = [C.POINTER(FusedDesc), C.c_void_p]

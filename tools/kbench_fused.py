@@ -13,7 +13,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 from paper_2603_23914_b200 import _capi as capi  # noqa: E402
-from test_gpu_fused import FusedDesc  # noqa: E402
+from paper_2603_23914_b200._capi import FusedDesc  # noqa: E402
 
 CONFIGS = {
     "c2": dict(B=16, H=32, Hkv=32, D=128, n=2304, rk=368, rv=368, nt=64 + 128, cap=320),
@@ -40,13 +40,18 @@ def main():
     bf = torch.bfloat16
     layers = []
     for _ in range(args.layers):
-        L = dict(lk=torch.randn(B, n, ld, device=dev).to(bf), lv=torch.randn(B, n, ld, device=dev).to(bf),
+        def packed(r):
+            src = torch.randn(B, n, r, device=dev).to(bf)
+            out = torch.empty(capi.lib().kvp_packed_left_bytes(B, n, r), dtype=torch.uint8, device=dev)
+            capi.call("kvp_pack_left", src.data_ptr(), r, B, n, r, out.data_ptr(), None)
+            return out
+        L = dict(lk=packed(rk), lv=packed(rv),
                  rk=(torch.randn(B, rk, W, device=dev) / W ** 0.5).to(bf),
                  rv=(torch.randn(B, rv, W, device=dev) / W ** 0.5).to(bf),
                  tk=torch.randn(B, cap, W, device=dev).to(bf), tv=torch.randn(B, cap, W, device=dev).to(bf),
                  q=torch.randn(B, H * D, device=dev), imp=torch.rand(B, n + cap, device=dev, dtype=torch.float64),
                  ctx=torch.empty(B, H * D, device=dev, dtype=bf))
-        L["desc"] = FusedDesc(H, Hkv, D, B, n, rk, rv, ld, cap, nt, None, args.cluster, 1, L["lk"].data_ptr(),
+        L["desc"] = FusedDesc(H, Hkv, D, B, n, rk, rv, 0, cap, nt, None, args.cluster, 1, L["lk"].data_ptr(),
                               L["rk"].data_ptr(), L["lv"].data_ptr(), L["rv"].data_ptr(), L["tk"].data_ptr(),
                               L["tv"].data_ptr(), L["q"].data_ptr(), L["imp"].data_ptr(), n + cap, 0.25, None,
                               L["ctx"].data_ptr())
