@@ -474,6 +474,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int i = it.lk0 + t * p.kpk + kp, s = i % NS;
           mbar_wait(&bars[kFull + s], (i / NS) & 1);
           tc_fence_after();
+          if (p.debug & 2) {  // timing experiment: release without MMAs
+            mbar_arrive(&bars[kEmpty + s]);
+            continue;
+          }
           for (int kk = 0; kk < 4; ++kk) {
             const uint64_t ad = smem_desc(ring + s * kStageBytes + kk * 32, 16, 1024, kSwizzle128B);
             const uint64_t bh = smem_desc(phi + kp * NP * 128 + kk * 32, 16, 1024, kSwizzle128B);
@@ -638,36 +642,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 3] = global_ns();
 
-    // ---- U readback (TMEM -> U_loc[h][r]); publish (m_loc, z_loc, U_loc) to the cluster
-    mbar_wait(&bars[kUFull], 0);
-    tc_fence_after();
-    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 4] = global_ns();
-    float* uloc = reinterpret_cast<float*>(smem + L.uloc);
-    for (int mt = 0; mt < p.mtiles; ++mt) {
-      const int r = mt * 128 + qd * 32 + lane;
-      for (int c0 = 0; c0 < gcols; c0 += 4) {
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (it.tiles > 0) tmem_ld4(tmem_row(s_cols + static_cast<uint32_t>(mt * NP + gbase + c0)), v);
-        for (int e = 0; e < 4; ++e) {
-          const int h = gbase + c0 + e;
-          if (h < H && r < p.s.rank_v) uloc[h * L.uloc_stride + r] = v[e];
-        }
-      }
-    }
+    // ---- publish (m_loc, z_loc); global statistics while the U MMAs still run
     if (tid == 0) fence_acq_rel_cluster();
     named_bar(kBarCompute, kComputeThreads);
-    if (tid < C) mbar_arrive_cluster(&bars[kUReady], static_cast<uint32_t>(tid));
-    mbar_wait_cluster(&bars[kUReady], 0);
-
-    // ---- global softmax statistics from the peers' (m, z)
+    if (tid < C) mbar_arrive_cluster(&bars[kStats], static_cast<uint32_t>(tid));
+    mbar_wait_cluster(&bars[kStats], 0);
     if (tid < H) {
       const int h = tid;
-      float mp[8], zp[8];
+      float mp[8], zq[8];
 #pragma unroll
       for (int peer = 0; peer < 8; ++peer)
         if (peer < C) {
           mp[peer] = ld_dsmem_f32(&m_loc[h], static_cast<uint32_t>(peer));
-          zp[peer] = ld_dsmem_f32(&z_loc[h], static_cast<uint32_t>(peer));
+          zq[peer] = ld_dsmem_f32(&z_loc[h], static_cast<uint32_t>(peer));
         }
       float mg = -INFINITY;
 #pragma unroll
@@ -679,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (peer < C) {
           const float sc = mp[peer] == -INFINITY ? 0.f : __expf(mp[peer] - mg);
           scale_c[peer * NP + h] = sc;
-          zg += zp[peer] * sc;
+          zg += zq[peer] * sc;
         }
       const float zi = 1.0f / zg;
       m_g[h] = mg;
@@ -687,6 +674,78 @@ __global__ void __launch_bounds__(kThreads, 1)
       f_me[h] = (m_loc[h] == -INFINITY ? 0.f : __expf(m_loc[h] - mg)) * zi;
     }
     named_bar(kBarCompute, kComputeThreads);
+
+    // ---- head-averaged attention + importance EMA (importance.cpp:33-65); S re-read
+    //      from TMEM concurrently with the U MMAs (disjoint TMEM columns)
+    float* ha_part = part;  // [4 groups][kMaxTilesEma][128]
+    const float inv_h = 1.0f / static_cast<float>(H);
+    for (int t = 0; t < it.tiles; ++t) {
+      const int row = qd * 32 + lane;
+      float hsum = 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < gcols; c0 += 4) {
+        float v[4];
+        tmem_ld4(tmem_row(static_cast<uint32_t>(t * NP + gbase + c0)), v);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int h = gbase + c0 + e;
+          if (h < H) hsum = fmaf(__expf(v[e] - m_loc[h]), f_me[h], hsum);
+        }
+      }
+      ha_part[cg * 128 + row] = hsum;
+      named_bar(kBarCompute, kComputeThreads);
+      if (tid < 128) {
+        const int tk = t * 128 + tid;
+        if (tk < it.chunk_len) {
+          const float ha = (ha_part[tid] + ha_part[128 + tid] + ha_part[256 + tid] + ha_part[384 + tid]) * inv_h;
+          const long gi = it.c_first + tk;
+          if (a.head_avg) a.head_avg[static_cast<long>(b) * (p.s.n_comp + p.s.tail_cap) + gi] = ha;
+          if (a.importance)
+            a.importance[static_cast<long>(b) * a.imp_stride + gi] =
+                __dadd_rn(__dmul_rn(a.ema_decay, imps[tk]), __dmul_rn(a.ema_blend, static_cast<double>(ha)));
+        }
+      }
+      named_bar(kBarCompute, kComputeThreads);
+    }
+    // tail tokens: normalised p -> workspace (for vsum), head average, EMA
+    for (int w = tid; w < it.n_tk * H; w += kComputeThreads) {
+      const int j = w % it.n_tk, h = w / it.n_tk;
+      a.ws_tail[(static_cast<long>(b) * H + h) * p.s.tail_cap + it.t_first + j] = stail[j * NP + h] * f_me[h];
+    }
+    for (int j = tid; j < it.n_tk; j += kComputeThreads) {
+      float hs = 0.f;
+      for (int h = 0; h < H; ++h) hs = fmaf(stail[j * NP + h], f_me[h], hs);
+      const float ha = hs * inv_h;
+      const long gi = p.s.n_comp + it.t_first + j;
+      if (a.head_avg) a.head_avg[static_cast<long>(b) * (p.s.n_comp + p.s.tail_cap) + gi] = ha;
+      if (a.importance)
+        a.importance[static_cast<long>(b) * a.imp_stride + gi] =
+            __dadd_rn(__dmul_rn(a.ema_decay, imps[p.chunk + j]), __dmul_rn(a.ema_blend, static_cast<double>(ha)));
+    }
+
+    // ---- U readback (TMEM -> U_loc[h][r]); publish U_loc to the cluster
+    mbar_wait(&bars[kUFull], 0);
+    tc_fence_after();
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 4] = global_ns();
+    float* uloc = reinterpret_cast<float*>(smem + L.uloc);
+    for (int mt = 0; mt < p.mtiles; ++mt) {
+      const int r = mt * 128 + qd * 32 + lane;
+#pragma unroll
+      for (int c0 = 0; c0 < gcols; c0 += 4) {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (it.tiles > 0) tmem_ld4(tmem_row(s_cols + static_cast<uint32_t>(mt * NP + gbase + c0)), v);
+        for (int e = 0; e < 4; ++e) {
+          const int h = gbase + c0 + e;
+          if (h < H && r < p.s.rank_v) uloc[h * L.uloc_stride + r] = v[e];
+        }
+      }
+    }
+    tc_fence_before();
+    if (tid == 0) fence_acq_rel_cluster();
+    named_bar(kBarCompute, kComputeThreads);
+    if (tid == 0) mbar_arrive(&bars[kTmemFree]);
+    if (tid < C) mbar_arrive_cluster(&bars[kUReady], static_cast<uint32_t>(tid));
+    mbar_wait_cluster(&bars[kUReady], 0);
 
     // ---- reduce-scatter U over the cluster: heads h = c, c + C, ...; U / z -> workspace
     const int r4 = L.uloc_stride / 4;
@@ -716,54 +775,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0) fence_acq_rel_cluster();
     named_bar(kBarCompute, kComputeThreads);
     if (tid < C) mbar_arrive_cluster(&bars[kDone], static_cast<uint32_t>(tid));
-
-    // ---- head-averaged attention + importance EMA (importance.cpp:33-65), S re-read from TMEM
-    float* ha_part = part;  // [4 groups][128] (part_m / part_s are dead)
-    const float inv_h = 1.0f / static_cast<float>(H);
-    for (int t = 0; t < it.tiles; ++t) {
-      const int row = qd * 32 + lane;
-      float hsum = 0.f;
-      for (int c0 = 0; c0 < gcols; c0 += 4) {
-        float v[4];
-        tmem_ld4(tmem_row(static_cast<uint32_t>(t * NP + gbase + c0)), v);
-        for (int e = 0; e < 4; ++e) {
-          const int h = gbase + c0 + e;
-          if (h < H) hsum = fmaf(__expf(v[e] - m_loc[h]), f_me[h], hsum);
-        }
-      }
-      ha_part[cg * 128 + row] = hsum;
-      named_bar(kBarCompute, kComputeThreads);
-      if (tid < 128) {
-        const int tk = t * 128 + tid;
-        if (tk < it.chunk_len) {
-          const float ha = (ha_part[tid] + ha_part[128 + tid] + ha_part[256 + tid] + ha_part[384 + tid]) * inv_h;
-          const long gi = it.c_first + tk;
-          if (a.head_avg) a.head_avg[static_cast<long>(b) * (p.s.n_comp + p.s.tail_cap) + gi] = ha;
-          if (a.importance)
-            a.importance[static_cast<long>(b) * a.imp_stride + gi] =
-                __dadd_rn(__dmul_rn(a.ema_decay, imps[tk]), __dmul_rn(a.ema_blend, static_cast<double>(ha)));
-        }
-      }
-      named_bar(kBarCompute, kComputeThreads);
-    }
-    tc_fence_before();
-    if (tid == 0) mbar_arrive(&bars[kTmemFree]);
-    // tail tokens: normalised p -> workspace (for vsum), head average, EMA
-    for (int w = tid; w < it.n_tk * H; w += kComputeThreads) {
-      const int j = w % it.n_tk, h = w / it.n_tk;
-      const float pn = stail[j * NP + h] * f_me[h];
-      a.ws_tail[(static_cast<long>(b) * H + h) * p.s.tail_cap + it.t_first + j] = pn;
-    }
-    for (int j = tid; j < it.n_tk; j += kComputeThreads) {
-      float hs = 0.f;
-      for (int h = 0; h < H; ++h) hs = fmaf(stail[j * NP + h], f_me[h], hs);
-      const float ha = hs * inv_h;
-      const long gi = p.s.n_comp + it.t_first + j;
-      if (a.head_avg) a.head_avg[static_cast<long>(b) * (p.s.n_comp + p.s.tail_cap) + gi] = ha;
-      if (a.importance)
-        a.importance[static_cast<long>(b) * a.imp_stride + gi] =
-            __dadd_rn(__dmul_rn(a.ema_decay, imps[p.chunk + j]), __dmul_rn(a.ema_blend, static_cast<double>(ha)));
-    }
     mbar_wait_cluster(&bars[kDone], 0);  // peers may still be reading my U_loc / stats
     if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 5] = global_ns();
   }
