@@ -1,7 +1,271 @@
-// Prefill compaction on the GPU (randomized truncated SVD, linalg.cpp:68-105).
+// Prefill-time compaction on the GPU: randomized truncated SVD of every
+// (instance, kind) visual segment of a layer, batched
+// (linalg.cpp:68-105 randomized_svd, compress_now decoder.cpp:619-628).
+//
+//   Omega  = gaussian(W x k, svd_seed, stream 0x72737664), k = min(R + p, min(T, W))
+//   Y      = A Omega;              Q = orth(Y)
+//   repeat q times:  Z = A^T Q; Q' = orth(Z); Y = A Q'; Q = orth(Y)
+//   B      = Q^T A  (k x W)
+//   C      = B B^T  (k x k, fp64)  ->  C = U diag(s^2) U^T
+//   left   = Q U_R diag(s_R)   (T x R, singular values folded in, linalg.cpp:95-99)
+//   right  = diag(1/s_R) U_R^T B   (R x W, orthonormal rows)
+// orth(Y) is shifted CholeskyQR2 (Gram, Cholesky, triangular solve, twice)
+// instead of the reference's Householder QR (Eigen::HouseholderQR): the same
+// column space, GEMM-shaped.  Round-1 implementation: the large products are
+// cuBLAS strided-batched GEMMs and the k x k Cholesky / symmetric eigensolve
+// are cuSOLVER batched routines; the Philox sketch, the latent-factor workload
+// generator, shifting, scaling and the packing into the decode layout are ours.
+#include <cublas_v2.h>
+#include <cuda_bf16.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
 #include "common.cuh"
 #include "compact.cuh"
+#include "decode_fused.cuh"
+#include "philox.cuh"
 
 namespace kvp {
-void compact_visual(kvp_engine*) { fail(KVP_ERR_PARAMETER, "compaction: not available yet (use factor_init = 1)"); }
+namespace {
+
+void blas_ok(cublasStatus_t s, const char* what) {
+  if (s != CUBLAS_STATUS_SUCCESS) fail(KVP_ERR_CUDA, std::string(what) + ": cuBLAS status " + std::to_string(s));
+}
+void solver_ok(cusolverStatus_t s, const char* what) {
+  if (s != CUSOLVER_STATUS_SUCCESS) fail(KVP_ERR_CUDA, std::string(what) + ": cuSOLVER status " + std::to_string(s));
+}
+
+template <typename T>
+__global__ void gaussian_kernel(T* out, long n, uint64_t seed, uint64_t stream, uint64_t offset, double scale) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = static_cast<T>(philox_gaussian(seed, stream, offset + i) * scale);
+}
+
+// z[t, i] *= decay^i (harness.cpp:96-103)
+__global__ void decay_cols_kernel(float* z, long rows, int r, double decay) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < rows * r) z[i] = static_cast<float>(static_cast<double>(z[i]) * pow(decay, static_cast<double>(i % r)));
+}
+
+// out[t, c] += noise * g  (harness.cpp:123-125)
+__global__ void add_noise_kernel(float* out, long n, double noise, uint64_t seed, uint64_t stream, uint64_t offset) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = static_cast<float>(static_cast<double>(out[i]) + noise * philox_gaussian(seed, stream, offset + i));
+}
+
+// G (k x k, column-major) += shift * trace(G)/k * I ; one block per matrix.
+__global__ void shift_diag_kernel(double* g, int k, double rel) {
+  double* m = g + static_cast<long>(blockIdx.x) * k * k;
+  __shared__ double tr;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < k; ++i) t += m[static_cast<long>(i) * k + i];
+    tr = t;
+  }
+  __syncthreads();
+  const double s = rel * tr / k + 1e-300;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) m[static_cast<long>(i) * k + i] += s;
+}
+
+__global__ void f32_to_f64_kernel(const float* in, double* out, long n) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[i];
+}
+__global__ void f64_to_f32_kernel(const double* in, float* out, long n) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = static_cast<float>(in[i]);
+}
+
+// From the ascending eigen-decomposition of C (k x k, column-major, eigvecs in
+// columns): Us[:, j] = U[:, k-1-j] * s_j and Ui[:, j] = U[:, k-1-j] / s_j for
+// the top R (descending) — fp32 column-major k x R.
+__global__ void ritz_kernel(const double* evec, const double* eval, int k, int R, float* us, float* ui, float* sv) {
+  const int m = blockIdx.x;
+  const double* U = evec + static_cast<long>(m) * k * k;
+  const double* w = eval + static_cast<long>(m) * k;
+  const double top = fmax(w[k - 1], 0.0);
+  for (int idx = threadIdx.x; idx < k * R; idx += blockDim.x) {
+    const int j = idx / k, i = idx % k;
+    const int src = k - 1 - j;
+    const double lam = fmax(w[src], 0.0);
+    const double s = sqrt(lam);
+    const double inv = (lam > top * 1e-28 && s > 0.0) ? 1.0 / s : 0.0;
+    const double u = U[static_cast<long>(src) * k + i];
+    us[static_cast<long>(m) * k * R + static_cast<long>(j) * k + i] = static_cast<float>(u * s);
+    ui[static_cast<long>(m) * k * R + static_cast<long>(j) * k + i] = static_cast<float>(u * inv);
+    if (i == 0 && sv) sv[static_cast<long>(m) * R + j] = static_cast<float>(s);
+  }
+}
+
+__global__ void to_bf16_rows_kernel(const float* in, __nv_bfloat16* out, long n) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __float2bfloat16_rn(in[i]);
+}
+
+unsigned grid_for(long n) { return static_cast<unsigned>((n + 255) / 256); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// Batched randomized SVD on row-major fp32 matrices.
+// ---------------------------------------------------------------------------
+struct SvdWork {
+  cublasHandle_t blas = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  cusolverDnParams_t params = nullptr;
+  cudaStream_t stream = nullptr;
+  std::vector<void*> bufs;
+  template <typename T>
+  T* get(size_t n) {
+    void* p = nullptr;
+    KVP_CUDA(cudaMallocAsync(&p, n * sizeof(T), stream));
+    bufs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  bool owns = true;
+  ~SvdWork() {
+    for (void* p : bufs) cudaFreeAsync(p, stream);
+    if (owns && params) cusolverDnDestroyParams(params);
+    if (owns && solver) cusolverDnDestroy(solver);
+  }
+};
+
+namespace {
+
+// Row-major C (m x n) = op(A) op(B), batched with strides (elements).
+void gemm_rm(SvdWork& w, bool ta, bool tb, int m, int n, int k, const float* a, long sa, const float* b, long sb,
+             float* c, long sc, int batch) {
+  const float one = 1.f, zero = 0.f;
+  // column-major: C^T (n x m) = op(B)^T (n x k) * op(A)^T (k x m)
+  const int lda = ta ? m : k, ldb = tb ? k : n;
+  blas_ok(cublasGemmStridedBatchedEx(w.blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, n, m, k,
+                                     &one, b, CUDA_R_32F, ldb, sb, a, CUDA_R_32F, lda, sa, &zero, c, CUDA_R_32F, n,
+                                     sc, batch, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
+          "gemm (compaction)");
+}
+
+// Orthonormal basis of the columns of Y (m x k row-major, batch) in place:
+// shifted CholeskyQR2.  Row-major Y (m x k) is column-major Y^T (k x m).
+void orth(SvdWork& w, float* y, int m, int k, int batch) {
+  float* g = w.get<float>(static_cast<size_t>(batch) * k * k);
+  double* gd = w.get<double>(static_cast<size_t>(batch) * k * k);
+  std::vector<double*> gp(batch);
+  std::vector<float*> yp(batch);
+  double** d_gp = w.get<double*>(batch);
+  float** d_yp = w.get<float*>(batch);
+  float* gf = w.get<float>(static_cast<size_t>(batch) * k * k);
+  int* info = w.get<int>(batch);
+  for (int i = 0; i < batch; ++i) {
+    gp[i] = gd + static_cast<size_t>(i) * k * k;
+    yp[i] = y + static_cast<size_t>(i) * m * k;
+  }
+  KVP_CUDA(cudaMemcpyAsync(d_gp, gp.data(), sizeof(double*) * batch, cudaMemcpyHostToDevice, w.stream));
+  std::vector<float*> gfp(batch);
+  for (int i = 0; i < batch; ++i) gfp[i] = gf + static_cast<size_t>(i) * k * k;
+  float** d_gfp = w.get<float*>(batch);
+  KVP_CUDA(cudaMemcpyAsync(d_gfp, gfp.data(), sizeof(float*) * batch, cudaMemcpyHostToDevice, w.stream));
+  KVP_CUDA(cudaMemcpyAsync(d_yp, yp.data(), sizeof(float*) * batch, cudaMemcpyHostToDevice, w.stream));
+  for (int pass = 0; pass < 2; ++pass) {
+    // G = Y^T Y (k x k, symmetric; row/column-major identical)
+    gemm_rm(w, true, false, k, k, m, y, static_cast<long>(m) * k, y, static_cast<long>(m) * k, g,
+            static_cast<long>(k) * k, batch);
+    const long nk = static_cast<long>(batch) * k * k;
+    f32_to_f64_kernel<<<grid_for(nk), 256, 0, w.stream>>>(g, gd, nk);
+    KVP_LAUNCHED();
+    shift_diag_kernel<<<batch, 256, 0, w.stream>>>(gd, k, pass == 0 ? 1e-5 : 1e-7);
+    KVP_LAUNCHED();
+    // G = L L^T (column-major lower)
+    solver_ok(cusolverDnDpotrfBatched(w.solver, CUBLAS_FILL_MODE_LOWER, k, d_gp, k, info, batch), "potrfBatched");
+    f64_to_f32_kernel<<<grid_for(nk), 256, 0, w.stream>>>(gd, gf, nk);
+    KVP_LAUNCHED();
+    // Row-major Y L^-T  <=>  column-major (Y^T) solved as  L X = Y^T  (left, lower, no transpose)
+    const float one = 1.f;
+    blas_ok(cublasStrsmBatched(w.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k,
+                               m, &one, d_gfp, k, d_yp, k, batch),
+            "trsmBatched");
+  }
+}
+
+}  // namespace
+
+void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const float* a, int batch, int T, int W,
+                            int rank, uint64_t seed, int oversampling, int power_iterations, float* left,
+                            float* right) {
+  // cuSOLVER handles are expensive to create: one per process, re-bound to the stream
+  static cusolverDnHandle_t solver = nullptr;
+  static cusolverDnParams_t params = nullptr;
+  if (!solver) {
+    solver_ok(cusolverDnCreate(&solver), "cusolverDnCreate");
+    solver_ok(cusolverDnCreateParams(&params), "cusolverDnCreateParams");
+  }
+  SvdWork w;
+  w.blas = blas;
+  w.stream = stream;
+  w.solver = solver;
+  w.params = params;
+  w.owns = false;
+  solver_ok(cusolverDnSetStream(w.solver, stream), "cusolverDnSetStream");
+  const int k = std::min(rank + oversampling, std::min(T, W));
+  const long sA = static_cast<long>(T) * W;
+  float* omega = w.get<float>(static_cast<size_t>(W) * k);
+  gaussian_kernel<float><<<grid_for(static_cast<long>(W) * k), 256, 0, stream>>>(omega, static_cast<long>(W) * k, seed,
+                                                                                   0x72737664ull, 0, 1.0);
+  KVP_LAUNCHED();
+  float* y = w.get<float>(static_cast<size_t>(batch) * T * k);
+  float* z = w.get<float>(static_cast<size_t>(batch) * W * k);
+  gemm_rm(w, false, false, T, k, W, a, sA, omega, 0, y, static_cast<long>(T) * k, batch);
+  orth(w, y, T, k, batch);
+  for (int it = 0; it < power_iterations; ++it) {
+    gemm_rm(w, true, false, W, k, T, a, sA, y, static_cast<long>(T) * k, z, static_cast<long>(W) * k, batch);
+    orth(w, z, W, k, batch);
+    gemm_rm(w, false, false, T, k, W, a, sA, z, static_cast<long>(W) * k, y, static_cast<long>(T) * k, batch);
+    orth(w, y, T, k, batch);
+  }
+  // B = Q^T A (k x W)
+  float* bm = w.get<float>(static_cast<size_t>(batch) * k * W);
+  gemm_rm(w, true, false, k, W, T, y, static_cast<long>(T) * k, a, sA, bm, static_cast<long>(k) * W, batch);
+  // C = B B^T in fp64
+  double* bd = w.get<double>(static_cast<size_t>(batch) * k * W);
+  const long nb = static_cast<long>(batch) * k * W;
+  f32_to_f64_kernel<<<grid_for(nb), 256, 0, stream>>>(bm, bd, nb);
+  KVP_LAUNCHED();
+  double* cd = w.get<double>(static_cast<size_t>(batch) * k * k);
+  {
+    const double one = 1.0, zero = 0.0;
+    // row-major B (k x W) = column-major B^T (W x k); C = B B^T = (B^T)^T (B^T)
+    blas_ok(cublasDgemmStridedBatched(blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, W, &one, bd, W, static_cast<long>(k) * W, bd,
+                                      W, static_cast<long>(k) * W, &zero, cd, k, static_cast<long>(k) * k, batch),
+            "dgemm (Gram)");
+  }
+  double* evals = w.get<double>(static_cast<size_t>(batch) * k);
+  int* info = w.get<int>(batch);
+  size_t dev_ws = 0, host_ws = 0;
+  solver_ok(cusolverDnXsyevBatched_bufferSize(w.solver, w.params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, k,
+                                              CUDA_R_64F, cd, k, CUDA_R_64F, evals, CUDA_R_64F, &dev_ws, &host_ws, batch),
+            "syevBatched_bufferSize");
+  void* dws = w.get<char>(std::max<size_t>(dev_ws, 16));
+  std::vector<char> hws(std::max<size_t>(host_ws, 16));
+  solver_ok(cusolverDnXsyevBatched(w.solver, w.params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, k, CUDA_R_64F,
+                                   cd, k, CUDA_R_64F, evals, CUDA_R_64F, dws, dev_ws, hws.data(), host_ws, info, batch),
+            "syevBatched");
+  // left = Q (U_R s), right = (U_R / s)^T B
+  float* us = w.get<float>(static_cast<size_t>(batch) * k * rank);
+  float* ui = w.get<float>(static_cast<size_t>(batch) * k * rank);
+  ritz_kernel<<<batch, 256, 0, stream>>>(cd, evals, k, rank, us, ui, nullptr);
+  KVP_LAUNCHED();
+  // us/ui are column-major k x R == row-major R x k (rows = components).
+  // left (T x R) = Q (T x k) * Us (k x R): Us row-major (k x R) is ui^T... build explicitly:
+  // row-major M (k x R) with M[i][j] = us_colmajor[j*k + i]  ->  op(B)=T on the R x k row-major view.
+  gemm_rm(w, false, true, T, rank, k, y, static_cast<long>(T) * k, us, static_cast<long>(k) * rank, left,
+          static_cast<long>(T) * rank, batch);
+  // right (R x W) = Ui^T (R x k, row-major view of ui) * B (k x W)
+  gemm_rm(w, false, false, rank, W, k, ui, static_cast<long>(k) * rank, bm, static_cast<long>(k) * W, right,
+          static_cast<long>(rank) * W, batch);
+  (void)hws;
+}
+
 }  // namespace kvp

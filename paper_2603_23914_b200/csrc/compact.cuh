@@ -1,10 +1,14 @@
-// Prefill-time compaction of the engine's visual segments (compact.cu).
+// Prefill-time compaction (compact.cu): batched randomized truncated SVD.
 #pragma once
 
-#include "kvp_b200.h"
+#include <cublas_v2.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
 
 namespace kvp {
-// Generates every layer's visual K/V prefill (latent-factor model, Philox) and
-// factors it in place into the engine's left/right buffers.
-void compact_visual(kvp_engine* e);
+// a: batch x (T x W) row-major fp32; left: batch x (T x rank), right: batch x (rank x W).
+void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const float* a, int batch, int T, int W,
+                            int rank, uint64_t seed, int oversampling, int power_iterations, float* left,
+                            float* right);
 }  // namespace kvp

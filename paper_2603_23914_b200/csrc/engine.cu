@@ -260,6 +260,123 @@ void enqueue_step(kvp_engine* e) {
   }
 }
 
+__global__ void gauss_f32_kernel(float* out, long n, uint64_t seed, uint64_t stream, uint64_t offset) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = static_cast<float>(philox_gaussian(seed, stream, offset + i));
+}
+
+// z[t, i] *= decay^i; loadings L_h = [shared ; head_h] per kv head (harness.cpp:96-113)
+__global__ void latent_prepare_kernel(float* z, long T, int r, double decay) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < T * r) z[i] = static_cast<float>(static_cast<double>(z[i]) * pow(decay, static_cast<double>(i % r)));
+}
+__global__ void latent_loadings_kernel(float* loads, int Hkv, int r, int shared, int D, uint64_t seed, uint64_t stream,
+                                       uint64_t base) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long n = static_cast<long>(Hkv) * r * D;
+  if (i >= n) return;
+  const int h = static_cast<int>(i / (static_cast<long>(r) * D));
+  const int row = static_cast<int>((i / D) % r), j = static_cast<int>(i % D);
+  const uint64_t idx = row < shared ? base + static_cast<uint64_t>(row) * D + j
+                                    : base + static_cast<uint64_t>(shared) * D +
+                                          (static_cast<uint64_t>(h) * (r - shared) + (row - shared)) * D + j;
+  loads[i] = static_cast<float>(philox_gaussian(seed, stream, idx));
+}
+__global__ void noise_kernel(float* out, long n, double noise, uint64_t seed, uint64_t stream, uint64_t base) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = static_cast<float>(static_cast<double>(out[i]) + noise * philox_gaussian(seed, stream, base + i));
+}
+__global__ void f32_to_bf16_kernel(const float* in, __nv_bfloat16* out, long n) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = __float2bfloat16_rn(in[i]);
+}
+
+// Visual prefill K/V of every instance of layer l, fp32 [2B][T][W] (K of b at 2b, V at 2b+1),
+// from the latent-factor model with the reference's Philox streams.
+void generate_visual(kvp_engine* e, int l, float* a, float* zbuf, float* lbuf) {
+  cudaStream_t s = e->stream;
+  const auto& pr = e->cfg.visual;
+  const int T = e->n, W = e->W, D = e->D, Hkv = e->Hkv;
+  const int r = pr.true_rank, sh = std::min(pr.shared_subspace, pr.true_rank);
+  const uint64_t seed = e->cfg.seed;
+  for (int b = 0; b < e->B; ++b)
+    for (int kind = 0; kind < 2; ++kind) {
+      const uint64_t st = stream_id(2, b, l, kind);
+      float* out = a + (static_cast<size_t>(b) * 2 + kind) * T * W;
+      const long nz = static_cast<long>(T) * r;
+      launch_1d(nz, [&](unsigned g, int t) { gauss_f32_kernel<<<g, t, 0, s>>>(zbuf, nz, seed, st, 0); });
+      launch_1d(nz, [&](unsigned g, int t) { latent_prepare_kernel<<<g, t, 0, s>>>(zbuf, T, r, pr.spectrum_decay); });
+      const long nl = static_cast<long>(Hkv) * r * D;
+      launch_1d(nl, [&](unsigned g, int t) {
+        latent_loadings_kernel<<<g, t, 0, s>>>(lbuf, Hkv, r, sh, D, seed, st, static_cast<uint64_t>(nz));
+      });
+      // out[:, h*D:(h+1)*D] = z (T x r) * L_h (r x D), batched over heads, ldc = W
+      const float one = 1.f, zero = 0.f;
+      blas_check(cublasGemmStridedBatchedEx(e->blas, CUBLAS_OP_N, CUBLAS_OP_N, D, T, r, &one, lbuf, CUDA_R_32F, D,
+                                            static_cast<long long>(r) * D, zbuf, CUDA_R_32F, r, 0, &zero, out,
+                                            CUDA_R_32F, W, D, Hkv, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
+                 "latent gemm");
+      if (pr.noise_floor > 0.0) {
+        const uint64_t nbase = static_cast<uint64_t>(nz) + static_cast<uint64_t>(sh) * D +
+                               static_cast<uint64_t>(Hkv) * (r - sh) * D;
+        const long n = static_cast<long>(T) * W;
+        launch_1d(n, [&](unsigned g, int t) { noise_kernel<<<g, t, 0, s>>>(out, n, pr.noise_floor, seed, st, nbase); });
+      }
+    }
+}
+
+}  // namespace
+
+// Prefill compaction (compress_now for the visual segment of every instance
+// and layer): generate K/V, randomized SVD, store bf16 factors in the decode
+// layout (left packed, right row-major).
+void compact_visual(kvp_engine* e) {
+  cudaStream_t s = e->stream;
+  const int T = e->n, W = e->W;
+  const int nb = 2 * e->B;
+  const auto& pr = e->cfg.visual;
+  float* a = nullptr;
+  float *zbuf = nullptr, *lbuf = nullptr, *left = nullptr, *right = nullptr;
+  __nv_bfloat16* lb = nullptr;
+  const int rmax = std::max(e->rk, e->rv);
+  KVP_CUDA(cudaMallocAsync(&a, sizeof(float) * nb * T * W, s));
+  KVP_CUDA(cudaMallocAsync(&zbuf, sizeof(float) * T * pr.true_rank, s));
+  KVP_CUDA(cudaMallocAsync(&lbuf, sizeof(float) * e->Hkv * pr.true_rank * e->D, s));
+  KVP_CUDA(cudaMallocAsync(&left, sizeof(float) * nb * T * rmax, s));
+  KVP_CUDA(cudaMallocAsync(&right, sizeof(float) * nb * rmax * W, s));
+  KVP_CUDA(cudaMallocAsync(&lb, sizeof(__nv_bfloat16) * nb * T * rmax, s));
+  require(e->rk == e->rv, KVP_ERR_PARAMETER, "engine compaction: rank_k must equal rank_v");
+  const int R = e->rk;
+  for (int l = 0; l < e->L; ++l) {
+    generate_visual(e, l, a, zbuf, lbuf);
+    randomized_svd_batched(e->blas, s, a, nb, T, W, R, e->cfg.svd_seed, e->cfg.svd_oversampling,
+                           e->cfg.svd_power_iterations, left, right);
+    // split K (even) / V (odd) matrices into the layer's buffers
+    for (int kind = 0; kind < 2; ++kind) {
+      for (int b = 0; b < e->B; ++b) {
+        const size_t m = static_cast<size_t>(b) * 2 + kind;
+        __nv_bfloat16* rdst = (kind == 0 ? e->rkf + static_cast<size_t>(l) * e->right_k_elems()
+                                         : e->rvf + static_cast<size_t>(l) * e->right_v_elems()) +
+                              static_cast<size_t>(b) * R * W;
+        const long nr = static_cast<long>(R) * W;
+        launch_1d(nr, [&](unsigned g, int t) { f32_to_bf16_kernel<<<g, t, 0, s>>>(right + m * R * W, rdst, nr); });
+        const long nlft = static_cast<long>(T) * R;
+        launch_1d(nlft, [&](unsigned g, int t) {
+          f32_to_bf16_kernel<<<g, t, 0, s>>>(left + m * T * R, lb + static_cast<size_t>(b) * T * R, nlft);
+        });
+      }
+      unsigned char* dst = kind == 0 ? e->lk + static_cast<size_t>(l) * e->lk_bytes()
+                                     : e->lv + static_cast<size_t>(l) * e->lv_bytes();
+      pack_left(lb, R, e->B, T, R, dst, s);
+    }
+  }
+  for (void* p : {static_cast<void*>(a), static_cast<void*>(zbuf), static_cast<void*>(lbuf), static_cast<void*>(left),
+                  static_cast<void*>(right), static_cast<void*>(lb)})
+    KVP_CUDA(cudaFreeAsync(p, s));
+}
+
+namespace {
+
 void build_graph(kvp_engine* e) {
   if (e->graph_exec) return;
   const uint64_t before = kvp_launch_count();
@@ -423,7 +540,7 @@ extern "C" int kvp_engine_prefill(kvp_engine* e) {
         }
       KVP_CUDA(cudaFreeAsync(scratch, s));
     } else {
-      compact_visual(e);
+      kvp::compact_visual(e);
     }
     KVP_CUDA(cudaEventRecord(e1, s));
     KVP_CUDA(cudaMemsetAsync(e->imp, 0, sizeof(double) * e->L * e->B * e->imp_stride(), s));
