@@ -41,14 +41,7 @@ struct kvp_engine {
   __nv_bfloat16 *xb = nullptr, *ctx = nullptr;
   float *qkv = nullptr, *q = nullptr, *xin = nullptr, *xcur = nullptr, *yout = nullptr;
   int* n_tail_dev = nullptr;
-  void* fused_ws = nullptr;
-  size_t fused_ws_bytes = 0;
-  kvp::FusedPlan plan{};   // whole batch (workspace, tensor maps)
-  kvp::FusedPlan gplan{};  // one instance group (launch grids)
-  int groups = 1;          // instance groups pipelined across two streams
-  int core_priority = 0;
-  cudaStream_t stream2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_q0 = nullptr, ev_join = nullptr;
+  kvp::LayerPlan lplan{};  // one-launch layer kernel
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   double compaction_ms = 0.0;
@@ -68,9 +61,6 @@ struct kvp_engine {
     if (graph) cudaGraphDestroy(graph);
     for (void* p : allocations) cudaFree(p);
     if (blas) cublasDestroy(blas);
-    for (cudaEvent_t ev : {ev_fork, ev_q0, ev_join})
-      if (ev) cudaEventDestroy(ev);
-    if (stream2) cudaStreamDestroy(stream2);
     if (stream) cudaStreamDestroy(stream);
   }
   size_t lk_bytes() const { return kvp::packed_left_bytes(B, n, rk); }  // per layer, packed
@@ -103,7 +93,8 @@ __global__ void gen_weight_kernel(__nv_bfloat16* out, long ld_out, int col0, int
 // consumed as z (T x r, latent i scaled by decay^i), shared loadings
 // (shared x D), per-head loadings (Hkv x (r - shared) x D), then noise (T x W).
 // out[t, h*D + j] = sum_i z[t,i] * load_h[i, j] + noise * g.
-__global__ void latent_direct_kernel(__nv_bfloat16* out, long ld_out, int T, int Hkv, int D, int r, int shared,
+// Written head-major: out[(h * rows_hm + t) * D + j] (the tail layout, kvp_pack_heads).
+__global__ void latent_direct_kernel(__nv_bfloat16* out, int rows_hm, int T, int Hkv, int D, int r, int shared,
                                      double decay, double noise, uint64_t seed, uint64_t stream) {
   const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int W = Hkv * D;
@@ -121,14 +112,14 @@ __global__ void latent_direct_kernel(__nv_bfloat16* out, long ld_out, int T, int
     sc *= decay;
   }
   if (noise > 0.0) acc += noise * philox_gaussian(seed, stream, base_n + static_cast<uint64_t>(t) * W + col);
-  out[static_cast<long>(t) * ld_out + col] = __float2bfloat16_rn(static_cast<float>(acc));
+  out[(static_cast<long>(h) * rows_hm + t) * D + j] = __float2bfloat16_rn(static_cast<float>(acc));
 }
 
 // Placeholder factors for factor_init = 1 (decode-only benchmarking): left
 // rows N(0,1) * 0.98^r (row-major scratch, packed afterwards), right rows
-// N(0,1)/sqrt(W) (near-orthonormal for W >> R).
-__global__ void synth_factor_kernel(__nv_bfloat16* left, int n, int rank, __nv_bfloat16* right, int W, uint64_t seed,
-                                    uint64_t stream) {
+// N(0,1)/sqrt(W) (near-orthonormal for W >> R), stored head-major.
+__global__ void synth_factor_kernel(__nv_bfloat16* left, int n, int rank, __nv_bfloat16* right, int W, int D,
+                                    uint64_t seed, uint64_t stream) {
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long nl = static_cast<long>(n) * rank, nr = static_cast<long>(rank) * W;
   if (i < nl) {
@@ -136,7 +127,9 @@ __global__ void synth_factor_kernel(__nv_bfloat16* left, int n, int rank, __nv_b
     left[i] = __float2bfloat16_rn(static_cast<float>(philox_gaussian(seed, stream, i) * pow(0.98, r)));
   } else if (i < nl + nr) {
     const long k = i - nl;
-    right[k] = __float2bfloat16_rn(static_cast<float>(philox_gaussian(seed, stream ^ 0x5A5Aull, k)) * rsqrtf(float(W)));
+    const long r = k / W, c = k % W;
+    right[((c / D) * rank + r) * D + c % D] =
+        __float2bfloat16_rn(static_cast<float>(philox_gaussian(seed, stream ^ 0x5A5Aull, k)) * rsqrtf(float(W)));
   }
 }
 
@@ -146,25 +139,6 @@ __global__ void to_bf16_kernel(const float* in, __nv_bfloat16* out, long n) {
 }
 
 __global__ void bump_counter_kernel(int* c) { *c += 1; }
-
-// Split [q | k | v] (fp32, B x (HD + 2W)); q -> q buffer, k/v -> bf16 tail row
-// (n_tail - 1), new token importance 0 (cache.cpp:147-170, importance.cpp:9-14).
-__global__ void append_kernel(const float* qkv, float* q, __nv_bfloat16* tk, __nv_bfloat16* tv, double* imp,
-                              const int* n_tail, int HD, int W, int cap, int n_comp, long imp_stride) {
-  const int b = blockIdx.y;
-  const int row = *n_tail - 1;
-  const float* src = qkv + static_cast<long>(b) * (HD + 2 * W);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HD + 2 * W; i += gridDim.x * blockDim.x) {
-    if (i < HD) {
-      q[static_cast<long>(b) * HD + i] = src[i];
-    } else if (i < HD + W) {
-      tk[(static_cast<long>(b) * cap + row) * W + (i - HD)] = __float2bfloat16_rn(src[i]);
-    } else {
-      tv[(static_cast<long>(b) * cap + row) * W + (i - HD - W)] = __float2bfloat16_rn(src[i]);
-    }
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) imp[static_cast<long>(b) * imp_stride + n_comp + row] = 0.0;
-}
 
 void launch_1d(long n, auto&& f) {
   const int threads = 256;
@@ -205,43 +179,12 @@ FusedArgs fused_args(kvp_engine* e, int l) {
   a.head_avg = nullptr;
   a.ctx_out = e->ctx;
   a.ctx_bf16 = 1;
-  a.ws_pimg = static_cast<unsigned char*>(e->fused_ws);
-  a.ws_tail = reinterpret_cast<float*>(a.ws_pimg + static_cast<size_t>(e->B) * 2 * e->plan.kpk * e->plan.np * 128);
-  a.ws_u = a.ws_tail + static_cast<size_t>(e->B) * e->H * e->cap;
   a.trace = nullptr;
   return a;
 }
 
-// Attention for one layer, instance groups pipelined over two streams:
-// qdots(g0) -> [core(g0) || qdots(g1)] -> [vsum(g0) || core(g1)] -> vsum(g1).
-void enqueue_attention(kvp_engine* e, int l) {
-  cudaStream_t s = e->stream;
-  const FusedArgs full = fused_args(e, l);
-  if (e->groups == 1) {
-    launch_qdots(e->gplan, full, s);
-    launch_core(e->gplan, full, s, e->core_priority);
-    launch_vsum(e->gplan, full, s);
-    return;
-  }
-  const int gb = e->gplan.s.batch;
-  KVP_CUDA(cudaEventRecord(e->ev_fork, s));
-  KVP_CUDA(cudaStreamWaitEvent(e->stream2, e->ev_fork, 0));
-  const FusedArgs a0 = offset_args(e->plan, full, 0);
-  launch_qdots(e->gplan, a0, s);
-  KVP_CUDA(cudaEventRecord(e->ev_q0, s));
-  launch_core(e->gplan, a0, s, e->core_priority);
-  launch_vsum(e->gplan, a0, s);
-  for (int g = 1; g < e->groups; ++g) {
-    const FusedArgs ag = offset_args(e->plan, full, g * gb);
-    KVP_CUDA(cudaStreamWaitEvent(e->stream2, e->ev_q0, 0));
-    launch_qdots(e->gplan, ag, e->stream2);
-    KVP_CUDA(cudaEventRecord(e->ev_q0, e->stream2));
-    launch_core(e->gplan, ag, e->stream2, e->core_priority);
-    launch_vsum(e->gplan, ag, e->stream2);
-  }
-  KVP_CUDA(cudaEventRecord(e->ev_join, e->stream2));
-  KVP_CUDA(cudaStreamWaitEvent(s, e->ev_join, 0));
-}
+// Attention for one layer: one cluster launch over the whole batch.
+void enqueue_attention(kvp_engine* e, int l) { launch_layer(e->lplan, fused_args(e, l), e->stream); }
 
 // One decode step over all layers, enqueued on e->stream (graph-capturable).
 void enqueue_step(kvp_engine* e) {
@@ -290,6 +233,13 @@ __global__ void f32_to_bf16_kernel(const float* in, __nv_bfloat16* out, long n) 
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) out[i] = __float2bfloat16_rn(in[i]);
 }
+// fp32 row-major [rows][W] -> bf16 head-major [W/D][rows][D]
+__global__ void f32_to_bf16_heads_kernel(const float* in, __nv_bfloat16* out, int rows, int W, int D) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<long>(rows) * W) return;
+  const long r = i / W, c = i % W;
+  out[((c / D) * rows + r) * D + c % D] = __float2bfloat16_rn(in[i]);
+}
 
 // Visual prefill K/V of every instance of layer l, fp32 [2B][T][W] (K of b at 2b, V at 2b+1),
 // from the latent-factor model with the reference's Philox streams.
@@ -329,7 +279,7 @@ void generate_visual(kvp_engine* e, int l, float* a, float* zbuf, float* lbuf) {
 
 // Prefill compaction (compress_now for the visual segment of every instance
 // and layer): generate K/V, randomized SVD, store bf16 factors in the decode
-// layout (left packed, right row-major).
+// layout (left packed, right head-major).
 void compact_visual(kvp_engine* e) {
   cudaStream_t s = e->stream;
   const int T = e->n, W = e->W;
@@ -359,7 +309,9 @@ void compact_visual(kvp_engine* e) {
                                          : e->rvf + static_cast<size_t>(l) * e->right_v_elems()) +
                               static_cast<size_t>(b) * R * W;
         const long nr = static_cast<long>(R) * W;
-        launch_1d(nr, [&](unsigned g, int t) { f32_to_bf16_kernel<<<g, t, 0, s>>>(right + m * R * W, rdst, nr); });
+        launch_1d(nr, [&](unsigned g, int t) {
+          f32_to_bf16_heads_kernel<<<g, t, 0, s>>>(right + m * R * W, rdst, R, W, e->D);
+        });
         const long nlft = static_cast<long>(T) * R;
         launch_1d(nlft, [&](unsigned g, int t) {
           f32_to_bf16_kernel<<<g, t, 0, s>>>(left + m * T * R, lb + static_cast<size_t>(b) * T * R, nlft);
@@ -426,23 +378,10 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     e->rv = std::min(c->rank_v, std::min(e->n, e->W));
     e->ld = 0;
     FusedShape fs{e->H, e->Hkv, e->D, e->n, e->rk, e->rv, e->ld, e->cap, e->B, c->cluster};
-    if (fs.cluster <= 0) fs.cluster = auto_cluster_size(fs);
-    e->plan = plan_fused(fs);
-    require(e->plan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->plan.why).c_str());
-    e->groups = 1;  // two-group pipelining measured slower on B200 (KVP_GROUPS to override)
-    if (const char* g = std::getenv("KVP_GROUPS")) e->groups = std::max(1, std::atoi(g));
-    require(e->B % e->groups == 0, KVP_ERR_PARAMETER, "engine: batch must divide into the instance groups");
-    FusedShape gs = fs;
-    gs.batch = e->B / e->groups;
-    e->gplan = plan_fused(gs);
-    require(e->gplan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->gplan.why).c_str());
-    int lo = 0, hi = 0;
-    KVP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    e->core_priority = hi;  // numerically lowest = highest priority
+    if (fs.cluster <= 0) fs.cluster = auto_layer_cluster(fs);
+    e->lplan = plan_layer(fs);
+    require(e->lplan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->lplan.why).c_str());
     KVP_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-    KVP_CUDA(cudaStreamCreateWithFlags(&e->stream2, cudaStreamNonBlocking));
-    for (cudaEvent_t* ev : {&e->ev_fork, &e->ev_q0, &e->ev_join})
-      KVP_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     blas_check(cublasCreate(&e->blas), "cublasCreate");
     blas_check(cublasSetStream(e->blas, e->stream), "cublasSetStream");
     const size_t blas_ws = 32u << 20;
@@ -466,9 +405,6 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     e->xcur = e->alloc<float>(static_cast<size_t>(e->B) * e->HD);
     e->yout = e->alloc<float>(static_cast<size_t>(e->B) * e->HD);
     e->n_tail_dev = e->alloc<int>(1);
-    e->fused_ws_bytes = fused_workspace_bytes(fs);
-    e->fused_ws = e->alloc<char>(e->fused_ws_bytes);
-    KVP_CUDA(cudaMemset(e->fused_ws, 0, e->fused_ws_bytes));
     *out = e.release();
   });
 }
@@ -508,7 +444,7 @@ extern "C" int kvp_engine_prefill(kvp_engine* e) {
                                  static_cast<size_t>(b) * e->cap * e->W;
             const auto& pr = e->cfg.textual;
             launch_1d(static_cast<long>(e->t0) * e->W, [&](unsigned g, int t) {
-              latent_direct_kernel<<<g, t, 0, s>>>(dst, e->W, e->t0, e->Hkv, e->D, pr.true_rank,
+              latent_direct_kernel<<<g, t, 0, s>>>(dst, e->cap, e->t0, e->Hkv, e->D, pr.true_rank,
                                                    std::min(pr.shared_subspace, pr.true_rank), pr.spectrum_decay,
                                                    pr.noise_floor, seed, stream_id(2, b, l, 2 + kind));
             });
@@ -531,7 +467,7 @@ extern "C" int kvp_engine_prefill(kvp_engine* e) {
                                    static_cast<size_t>(b) * rank * e->W;
             launch_1d(static_cast<long>(e->n) * rank + static_cast<long>(rank) * e->W, [&](unsigned g, int t) {
               synth_factor_kernel<<<g, t, 0, s>>>(scratch + static_cast<size_t>(b) * e->n * rank, e->n, rank, right,
-                                                  e->W, seed, stream_id(2, b, l, kind));
+                                                  e->W, e->D, seed, stream_id(2, b, l, kind));
             });
           }
           unsigned char* dst = kind == 0 ? e->lk + static_cast<size_t>(l) * e->lk_bytes()
@@ -606,7 +542,7 @@ extern "C" int kvp_engine_get_info(kvp_engine* e, kvp_engine_info* info) {
   return guarded([&] {
     require(e && info, KVP_ERR_PARAMETER, "engine: null argument");
     std::memset(info, 0, sizeof(*info));
-    info->cluster = e->plan.s.cluster;
+    info->cluster = e->lplan.s.cluster;
     info->rank_k = e->rk;
     info->rank_v = e->rv;
     info->ld_left = e->ld;
@@ -670,7 +606,7 @@ extern "C" int kvp_engine_time_attention(kvp_engine* e, int32_t iters, double* m
     KVP_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;
     KVP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    note_launch(static_cast<uint64_t>(iters + 1) * e->L * 3);
+    note_launch(static_cast<uint64_t>(iters + 1) * e->L);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaGraphExecDestroy(ge);

@@ -53,10 +53,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
-// Acquire at cluster scope: pairs with remote release-arrives.
+// Acquire at cluster scope: pairs with remote release-arrives.  Backs off
+// between polls: a tight cluster-scope acquire loop slows the SM's streams.
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   uint32_t ok = 0;
-  while (!ok) {
+  for (int spin = 0; !ok; ++spin) {
+    if (spin > 0) __nanosleep(256);
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
@@ -74,6 +76,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
           smem_addr(dst)),
       "l"(map), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int32_t c0, int32_t c1, int32_t c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar))
       : "memory");
 }
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -113,6 +123,17 @@ __device__ __forceinline__ uint4 ld_dsmem_v4(const void* local, uint32_t cta) {
       : "memory");
   return v;
 }
+// 16-byte store to the same smem offset in CTA `cta` of the cluster.
+__device__ __forceinline__ void st_dsmem_v4(void* local, uint32_t cta, const uint4& v) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\t"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+      "st.shared::cluster.v4.u32 [ra], {%2, %3, %4, %5};\n\t}" ::"r"(smem_addr(local)),
+      "r"(cta), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+      : "memory");
+}
+// Generic-proxy writes (any state space) ordered before later async-proxy accesses.
+__device__ __forceinline__ void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 __device__ __forceinline__ float ld_dsmem_f32(const void* local, uint32_t cta) {
   float v;
   asm volatile(

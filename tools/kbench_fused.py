@@ -17,6 +17,9 @@ from paper_2603_23914_b200._capi import FusedDesc  # noqa: E402
 
 CONFIGS = {
     "c2": dict(B=16, H=32, Hkv=32, D=128, n=2304, rk=368, rv=368, nt=64 + 128, cap=320),
+    "c2b1": dict(B=1, H=32, Hkv=32, D=128, n=2304, rk=368, rv=368, nt=64 + 128, cap=320),
+    "c2b4": dict(B=4, H=32, Hkv=32, D=128, n=2304, rk=368, rv=368, nt=64 + 128, cap=320),
+    "c2r384": dict(B=16, H=32, Hkv=32, D=128, n=2304, rk=384, rv=384, nt=64 + 128, cap=320),
     "c3": dict(B=64, H=40, Hkv=40, D=128, n=4096, rk=284, rv=284, nt=64 + 128, cap=320),
     "c5": dict(B=32, H=32, Hkv=32, D=128, n=2048, rk=128, rv=128, nt=64 + 128, cap=320),
     "c4_8x": dict(B=16, H=32, Hkv=32, D=128, n=4096, rk=256, rv=256, nt=64 + 128, cap=320),
@@ -70,19 +73,30 @@ def main():
     torch.cuda.synchronize()
     if args.trace:
         cl = args.cluster or 8  # trace buffer sized for the largest cluster
-        buf = torch.zeros(B * cl * 16, dtype=torch.int64, device=dev)
+        buf = torch.zeros(B * cl * 16 + 3 * 2048 + 2 * 2048, dtype=torch.int64, device=dev)
         capi.lib().kvp_debug_fused_trace.argtypes = [C.c_void_p]
         capi.lib().kvp_debug_fused_trace(buf.data_ptr())
         capi.check(fn(C.byref(layers[0]["desc"]), stream))
         torch.cuda.synchronize()
         capi.lib().kvp_debug_fused_trace(None)
         capi.lib().kvp_debug_fused_max_clusters.argtypes = [C.POINTER(FusedDesc)]
-        print("max active clusters:", capi.lib().kvp_debug_fused_max_clusters(C.byref(layers[0]["desc"])))
-        t = buf.view(B * cl, 16)[:, :11].double().cpu()
+        capi.lib().kvp_debug_fused_cluster.argtypes = [C.POINTER(FusedDesc)]
+        print("cluster", capi.lib().kvp_debug_fused_cluster(C.byref(layers[0]["desc"])), "max active clusters:",
+              capi.lib().kvp_debug_fused_max_clusters(C.byref(layers[0]["desc"])))
+        it = buf[B * cl * 16:B * cl * 16 + 3 * 512].view(-1, 3).double().cpu()
+        it = it[it[:, 0] > 0]
+        if it.shape[0]:
+            t00 = it[0, 0].item()
+            print("block 0 items (SM clocks since first issue): issue / acquire / release-acquire, acquire-issue")
+            for k in range(it.shape[0]):
+                r = it[k] - t00
+                rel = (it[k, 2] - it[k, 1]).item() if it[k, 2] > 0 else float("nan")
+                print(f"  {k:4d} {r[0].item():9.0f} {r[1].item():9.0f} {rel:7.0f}   {(r[1] - r[0]).item():7.0f}")
+        t = buf[:B * cl * 16].view(B * cl, 16)[:, :11].double().cpu()
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
-        names = ["start", "S ready", "local stats", "p tiles", "U ready", "end", "stats tmem", "stats bar",
-                 "mma P ok", "mma S done", "prod LV0"]
+        names = ["start", "A pushed", "S ready", "p tiles", "U ready", "U reduced", "D done", "prod done",
+                 "mma P ok", "-", "-"]
         rel = (t - t0) / 1000.0
         print("phase (us since first CTA start): median / max over CTAs")
         for k, n_ in enumerate(names):

@@ -18,11 +18,12 @@ constexpr int kStage = 16384;
 
 template <int MODE>
 __global__ void __launch_bounds__(1024, 1) stream_kernel(const __grid_constant__ CUtensorMap map, const char* src,
-                                                        long bytes_per_cta, int stages, unsigned long long* sink, int panels) {
+                                                        long bytes_per_cta, int stages, unsigned long long* sink, int panels,
+                                                        int gap, int variant, int sb, long cta_stride) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * kStage);
-  const long n_items = bytes_per_cta / kStage;
-  const char* base = src + blockIdx.x * bytes_per_cta;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + stages * kStage);  // [stages] full (+ [stages] empty)
+  const long n_items = bytes_per_cta / (kStage + gap);
+  const char* base = src + blockIdx.x * (cta_stride ? cta_stride : bytes_per_cta);
   if (MODE == 3) {  // qdots pattern: block = 256-byte column slice (one head) of an [rows x 8 KB] matrix
     const int slice = blockIdx.x % 32, inst = blockIdx.x / 32;
     const long row_bytes = 8192, rows = bytes_per_cta / 256;  // same bytes per block as the other modes
@@ -58,6 +59,50 @@ __global__ void __launch_bounds__(1024, 1) stream_kernel(const __grid_constant__
     if (acc == 0x12345) sink[0] = acc;
     return;
   }
+  if (MODE == 4) {  // warp-specialised: warp 0 produces, warps 2.. consume
+    const long n_items = bytes_per_cta / (sb + gap);
+    full = reinterpret_cast<uint64_t*>(smem + stages * sb);
+    uint64_t* empty = full + stages;
+    const int nwarps = (blockDim.x - 64) / 32;
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < stages; ++s) {
+        mbar_init(&full[s], 1);
+        mbar_init(&empty[s], variant == 0 ? 1 : nwarps);
+      }
+      fence_mbar_init();
+    }
+    __syncthreads();
+    const int nthr = blockDim.x - 64;
+    if (threadIdx.x == 0) {
+      for (long i = 0; i < n_items; ++i) {
+        const int s = i % stages;
+        mbar_wait(&empty[s], ((i / stages) & 1) ^ 1);
+        mbar_expect_tx(&full[s], sb);
+        bulk_load(smem + s * sb, base + i * (sb + gap), sb, &full[s]);
+      }
+    } else if (threadIdx.x >= 64) {
+      const int tid = threadIdx.x - 64;
+      unsigned acc = 0;
+      for (long i = 0; i < n_items; ++i) {
+        const int s = i % stages;
+        if (variant == 0) {
+          if (tid == 0) mbar_wait(&full[s], (i / stages) & 1);
+          named_bar(1, nthr);
+          if (panels > 1) acc ^= reinterpret_cast<const unsigned*>(smem + s * kStage)[tid];
+          named_bar(1, nthr);
+          if (tid == 0) mbar_arrive(&empty[s]);
+        } else {
+          if (variant == 2 || (tid & 31) == 0) mbar_wait(&full[s], (i / stages) & 1);
+          __syncwarp();
+          if (panels > 1) acc ^= reinterpret_cast<const unsigned*>(smem + s * kStage)[tid];
+          __syncwarp();
+          if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+        }
+      }
+      if (acc == 0x12345) sink[0] = acc;
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) mbar_init(&full[s], 1);
     fence_mbar_init();
@@ -79,9 +124,17 @@ __global__ void __launch_bounds__(1024, 1) stream_kernel(const __grid_constant__
           const long tile = i / panels, panel = i % panels;
           tma_load_2d(dst, &map, static_cast<int>(panel * 64), static_cast<int>((row0 / panels) + tile * 128), &full[s]);
         }
-        else bulk_load(dst, base + i * kStage, kStage, &full[s]);
+        else bulk_load(dst, base + i * (kStage + gap), kStage, &full[s]);
       }
     }
+  }
+}
+
+__global__ void fill_kernel(unsigned* p, long n) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    unsigned x = static_cast<unsigned>(i) * 2654435761u + 0x9E3779B9u;
+    x ^= x >> 15; x *= 2246822519u; x ^= x >> 13; x *= 3266489917u; x ^= x >> 16;
+    p[i] = x;
   }
 }
 
@@ -94,6 +147,10 @@ int main(int argc, char** argv) {
   char* buf;
   cudaMalloc(&buf, per * ctas);
   cudaMemset(buf, 1, per * ctas);
+  if (getenv("RANDOM_FILL")) {  // incompressible contents
+    fill_kernel<<<1024, 256>>>(reinterpret_cast<unsigned*>(buf), per * ctas / 4);
+    cudaDeviceSynchronize();
+  }
   unsigned long long* sink;
   cudaMalloc(&sink, 8);
   PFN_cuTensorMapEncodeTiled_v12000 enc;
@@ -105,30 +162,51 @@ int main(int argc, char** argv) {
   const cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
   enc(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  const size_t smem = stages * kStage + 1024;
+  const size_t smem = stages * (argc > 12 ? atoi(argv[12]) : kStage) + 1024 + (argc > 8 ? atoi(argv[8]) : 0);
   cudaFuncSetAttribute(stream_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(stream_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(stream_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(stream_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const char* names[4] = {"tma2d", "bulk1d", "ldg128", "slice"};
+  cudaFuncSetAttribute(stream_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const char* names[5] = {"tma2d", "bulk1d", "ldg128", "slice", "wspec"};
   const int mode0 = argc > 5 ? atoi(argv[5]) : 0;
-  for (int mode = mode0; mode < 4; ++mode) {
-    auto k = mode == 0 ? stream_kernel<0> : mode == 1 ? stream_kernel<1> : mode == 2 ? stream_kernel<2> : stream_kernel<3>;
+  const int mode1 = argc > 9 ? atoi(argv[9]) : 4;
+  for (int mode = mode0; mode < mode1; ++mode) {
+    auto k = mode == 0 ? stream_kernel<0> : mode == 1 ? stream_kernel<1> : mode == 2 ? stream_kernel<2> : mode == 3 ? stream_kernel<3> : stream_kernel<4>;
     const dim3 grid(ctas);
     const int panels = row_elems / 64;
-    const int nthr = mode >= 2 ? ldg_threads : 128;
-    for (int rep = 0; rep < 2; ++rep) k<<<grid, nthr, smem>>>(map, buf, per, stages, sink, panels);
+    const int nthr = argc > 11 ? atoi(argv[11]) : mode == 4 ? 576 : mode >= 2 ? ldg_threads : 128;
+    const int csz = argc > 6 ? atoi(argv[6]) : 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(nthr);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = csz;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int gap = argc > 7 ? atoi(argv[7]) : 0;
+    const int variant = argc > 10 ? atoi(argv[10]) : 0;
+    const int sb = argc > 12 ? atoi(argv[12]) : kStage;
+    const long cta_stride = argc > 13 ? atol(argv[13]) : 0;
+    const long per_run = argc > 14 ? atol(argv[14]) : per;
+    auto launch = [&] { cudaLaunchKernelEx(&cfg, k, map, (const char*)buf, per_run, stages, sink, panels, gap, variant, sb, cta_stride); };
+    for (int rep = 0; rep < 2; ++rep) launch();
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    for (int rep = 0; rep < 5; ++rep) k<<<grid, nthr, smem>>>(map, buf, per, stages, sink, panels);
+    for (int rep = 0; rep < 5; ++rep) launch();
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
     cudaEventElapsedTime(&ms, e0, e1);
-    const double gbs = 5.0 * per * ctas / (ms * 1e-3) / 1e9;
-    printf("%-7s thr=%4d ctas=%3d stages=%2d  total %7.1f GB/s  per-CTA %6.1f GB/s  (%s)\n", names[mode], nthr, ctas, stages, gbs,
+    const double moved = mode == 4 ? static_cast<double>(per_run / (sb + gap)) * sb : static_cast<double>(per_run);
+    const double gbs = 5.0 * moved * ctas / (ms * 1e-3) / 1e9;
+    printf("csz=%d %-7s thr=%4d ctas=%3d stages=%2d  total %7.1f GB/s  per-CTA %6.1f GB/s  (%s)\n", csz, names[mode], nthr, ctas, stages, gbs,
            gbs / ctas, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
