@@ -159,9 +159,12 @@ int kvp_pack_heads(const void* src, void* dst, int32_t batch, int32_t rows, int3
                    int32_t to_heads, void* stream);
 
 /* One layer of a batch of caches in the serving layout: every instance holds
- * one factored block of n_comp tokens (left_k/left_v packed, see above;
- * right_k / right_v head-major [batch][kv_heads][rank][head_dim]) and a dense
- * tail (tail_k/tail_v head-major [batch][kv_heads][tail_cap][head_dim], n_tail rows valid — read from
+ * one factored block of n_comp tokens (left_k/left_v packed, see above) and a
+ * dense tail.  right_k / right_v ([rank][kv_heads*head_dim] per instance) and
+ * tail_k / tail_v ([tail_cap][kv_heads*head_dim]) are stored per kv head in the
+ * same packed row-tile layout: kvp_pack_heads to head-major, then kvp_pack_left
+ * with batch = batch*kv_heads, n = rows, rank = head_dim (head_dim 64 or 128).
+ * n_tail rows of the tail are valid — read from
  * n_tail_dev when non-NULL so the call can live in a CUDA graph).  This is
  * the plan build_retrieval_plan produces for the reference's default
  * configuration (visual block factored, textual tail dense; decoder.cpp:141-188)
@@ -246,7 +249,8 @@ typedef struct {
 } kvp_engine_info;
 
 /* Device pointers of one layer's state (for tests / inspection): left factors
- * packed (kvp_pack_left), right factors and tails head-major (kvp_pack_heads). */
+ * packed (kvp_pack_left), right factors and tails in the packed row-tile layout
+ * of kvp_decode_fused. */
 typedef struct {
   const void *left_k, *left_v, *right_k, *right_v, *tail_k, *tail_v;
   const double* importance;

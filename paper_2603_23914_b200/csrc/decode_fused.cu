@@ -5,6 +5,7 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <memory>
 #include <cstdlib>
 #include <string>
 
@@ -116,10 +117,17 @@ extern "C" int kvp_debug_fused_cluster(const kvp_fused_desc* d) {
   return n;
 }
 
-// The layer kernel keeps P, U and the tail weights on chip: no workspace.
+// Exchange area of the CTA groups (P image, statistics, U partials, context).
 extern "C" size_t kvp_decode_fused_workspace(const kvp_fused_desc* d) {
-  (void)d;
-  return 0;
+  size_t n = 0;
+  kvp::guarded([&] {
+    kvp::FusedShape s{d->heads, d->kv_heads, d->head_dim, d->n_comp, d->rank_k, d->rank_v, 0, d->tail_cap, d->batch,
+                      d->cluster};
+    if (s.cluster <= 0) s.cluster = kvp::auto_layer_cluster(s);
+    const kvp::LayerPlan lp = kvp::plan_layer(s);
+    if (lp.ok) n = kvp::layer_group_ws_bytes(lp);
+  });
+  return n;
 }
 
 extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
@@ -162,6 +170,16 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     a.ctx_out = d->context;
     a.ctx_bf16 = d->context_bf16;
     a.trace = g_trace;
+    const size_t ws_bytes = layer_group_ws_bytes(lp);
+    std::unique_ptr<Scratch> own;
+    if (d->workspace == nullptr) {  // stream-ordered scratch, barrier words zeroed
+      own = std::make_unique<Scratch>(ws_bytes, as_stream(stream));
+      KVP_CUDA(cudaMemsetAsync(own->p, 0, ws_bytes, as_stream(stream)));
+      a.group_ws = own->as<unsigned char>();
+    } else {
+      require(d->workspace_bytes >= ws_bytes, KVP_ERR_PARAMETER, "decode_fused: workspace too small");
+      a.group_ws = static_cast<unsigned char*>(d->workspace);
+    }
     launch_layer(lp, a, as_stream(stream));
   });
 }

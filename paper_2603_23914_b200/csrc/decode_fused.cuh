@@ -18,7 +18,7 @@ struct FusedShape {
   int ld_left;        // unused (left factors are packed)
   int tail_cap;       // tail rows allocated per instance
   int batch;
-  int cluster;        // CTAs per instance (one thread-block cluster)
+  int cluster;        // CTAs per instance (one co-resident group exchanging through L2)
 };
 
 struct FusedArgs {
@@ -27,9 +27,11 @@ struct FusedArgs {
   // XOR-swizzled by row % 8 (the tcgen05 SWIZZLE_128B K-major operand layout)
   const unsigned char* left_k_packed;  // [batch][ntiles][kpk][16 KB]
   const unsigned char* left_v_packed;  // [batch][ntiles][vpanels_st][16 KB]
-  const __nv_bfloat16* right_k;  // head-major [batch][Hkv][rank_k][D]
-  const __nv_bfloat16* right_v;  // head-major [batch][Hkv][rank_v][D]
-  const __nv_bfloat16* tail_k;   // head-major [batch][Hkv][tail_cap][D]
+  // right factors and tails: packed row tiles per kv head (pack_left layout of the head-major
+  // [batch*Hkv][rows][D] matrix): [batch*Hkv][ceil(rows/128)][D/64][16 KB]
+  const __nv_bfloat16* right_k;  // rows = rank_k
+  const __nv_bfloat16* right_v;  // rows = rank_v
+  const __nv_bfloat16* tail_k;   // rows = tail_cap
   const __nv_bfloat16* tail_v;
   const int* n_tail_dev;         // device counter of valid tail rows (nullable)
   int n_tail;                    // used when n_tail_dev == nullptr
@@ -44,6 +46,8 @@ struct FusedArgs {
   float* head_avg;               // [batch][n_comp + tail_cap] (nullable)
   void* ctx_out;                 // [batch][H*D]
   int ctx_bf16;                  // 1: bf16 output, 0: fp32
+  unsigned char* group_ws;       // [batch][layer_group_ws_bytes / batch] exchange area; its barrier
+                                 // words (first 8 bytes per instance) zeroed once at allocation
   unsigned long long* trace;     // debug: per-CTA phase timestamps [grid][16] (nullable)
 };
 
@@ -67,7 +71,11 @@ struct LayerPlan {
   int tpc;         // tail tokens per CTA in the tail EMA
   int stages;      // TMA ring stages (even)
   int tmem_cols;
-  int debug;       // timing experiments only (KVP_LAYER_DEBUG): 1 = skip phase A/D arithmetic
+  int nab;         // phase-A TMEM result buffers
+  int nob;         // phase-D operand buffers
+  int a_col, d_col;  // TMEM column of the phase-A buffers / phase-D accumulators
+  int debug;       // timing experiments only (KVP_LAYER_DEBUG): 8 = phase A only
+  int prefetch;    // L2 prefetch distance beyond the ring, in items
   size_t smem_bytes;
   bool ok;
   const char* why;
@@ -75,6 +83,7 @@ struct LayerPlan {
 LayerPlan plan_layer(const FusedShape& s);
 int auto_layer_cluster(FusedShape s);
 int layer_max_active_clusters(const LayerPlan& p);
+size_t layer_group_ws_bytes(const LayerPlan& p);
 void launch_layer(const LayerPlan& p, const FusedArgs& a, cudaStream_t st);
 
 }  // namespace kvp

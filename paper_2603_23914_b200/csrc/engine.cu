@@ -26,6 +26,7 @@
 #include "decode_fused.cuh"
 #include "engine.cuh"
 #include "philox.cuh"
+#include "sm100.cuh"
 
 struct kvp_engine {
   kvp_engine_config cfg{};
@@ -42,6 +43,7 @@ struct kvp_engine {
   float *qkv = nullptr, *q = nullptr, *xin = nullptr, *xcur = nullptr, *yout = nullptr;
   int* n_tail_dev = nullptr;
   kvp::LayerPlan lplan{};  // one-launch layer kernel
+  unsigned char* group_ws = nullptr;  // its L2 exchange area (shared by the layers: launches serialise)
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   double compaction_ms = 0.0;
@@ -65,9 +67,12 @@ struct kvp_engine {
   }
   size_t lk_bytes() const { return kvp::packed_left_bytes(B, n, rk); }  // per layer, packed
   size_t lv_bytes() const { return kvp::packed_left_bytes(B, n, rv); }
-  size_t right_k_elems() const { return static_cast<size_t>(B) * rk * W; }
-  size_t right_v_elems() const { return static_cast<size_t>(B) * rv * W; }
-  size_t tail_elems() const { return static_cast<size_t>(B) * cap * W; }
+  // right factors and tails: packed 128-row tiles per kv head (kvp_pack_left layout of the
+  // head-major [B*Hkv][rows][D] matrices)
+  static size_t tiles(int rows) { return static_cast<size_t>((rows + 127) / 128); }
+  size_t right_k_elems() const { return static_cast<size_t>(B) * Hkv * tiles(rk) * 128 * D; }
+  size_t right_v_elems() const { return static_cast<size_t>(B) * Hkv * tiles(rv) * 128 * D; }
+  size_t tail_elems() const { return static_cast<size_t>(B) * Hkv * tiles(cap) * 128 * D; }
   size_t imp_stride() const { return static_cast<size_t>(n) + cap; }
 };
 
@@ -76,6 +81,15 @@ namespace {
 
 void blas_check(cublasStatus_t s, const char* what) {
   if (s != CUBLAS_STATUS_SUCCESS) fail(KVP_ERR_CUDA, std::string(what) + ": cuBLAS status " + std::to_string(s));
+}
+
+// Element offset of (row r, column c = g*D + d) of one instance's [rows][Hkv*D]
+// matrix in the packed row-tile layout: tile (g, r / 128), 64-column panel d / 64,
+// 128-byte row r % 128 with 16-byte chunks XOR-swizzled by the row (sm100::sw128_off).
+__device__ __forceinline__ long packed_row_off(long r, int c, int D, int tiles_per_head) {
+  const int g = c / D, d = c % D;
+  const long tile = static_cast<long>(g) * tiles_per_head + r / 128;
+  return (tile * (D / 64) + d / 64) * 8192 + kvp::sm100::sw128_off(static_cast<uint32_t>(r % 128), d % 64) / 2;
 }
 
 // W ~ N(0,1) / sqrt(HD) from the reference's weight streams (harness.cpp:138-151):
@@ -93,8 +107,8 @@ __global__ void gen_weight_kernel(__nv_bfloat16* out, long ld_out, int col0, int
 // consumed as z (T x r, latent i scaled by decay^i), shared loadings
 // (shared x D), per-head loadings (Hkv x (r - shared) x D), then noise (T x W).
 // out[t, h*D + j] = sum_i z[t,i] * load_h[i, j] + noise * g.
-// Written head-major: out[(h * rows_hm + t) * D + j] (the tail layout, kvp_pack_heads).
-__global__ void latent_direct_kernel(__nv_bfloat16* out, int rows_hm, int T, int Hkv, int D, int r, int shared,
+// Written in the packed tail layout (rows_cap rows per kv head).
+__global__ void latent_direct_kernel(__nv_bfloat16* out, int rows_cap, int T, int Hkv, int D, int r, int shared,
                                      double decay, double noise, uint64_t seed, uint64_t stream) {
   const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int W = Hkv * D;
@@ -112,7 +126,7 @@ __global__ void latent_direct_kernel(__nv_bfloat16* out, int rows_hm, int T, int
     sc *= decay;
   }
   if (noise > 0.0) acc += noise * philox_gaussian(seed, stream, base_n + static_cast<uint64_t>(t) * W + col);
-  out[(static_cast<long>(h) * rows_hm + t) * D + j] = __float2bfloat16_rn(static_cast<float>(acc));
+  out[packed_row_off(t, col, D, (rows_cap + 127) / 128)] = __float2bfloat16_rn(static_cast<float>(acc));
 }
 
 // Placeholder factors for factor_init = 1 (decode-only benchmarking): left
@@ -128,7 +142,7 @@ __global__ void synth_factor_kernel(__nv_bfloat16* left, int n, int rank, __nv_b
   } else if (i < nl + nr) {
     const long k = i - nl;
     const long r = k / W, c = k % W;
-    right[((c / D) * rank + r) * D + c % D] =
+    right[packed_row_off(r, static_cast<int>(c), D, (rank + 127) / 128)] =
         __float2bfloat16_rn(static_cast<float>(philox_gaussian(seed, stream ^ 0x5A5Aull, k)) * rsqrtf(float(W)));
   }
 }
@@ -179,12 +193,15 @@ FusedArgs fused_args(kvp_engine* e, int l) {
   a.head_avg = nullptr;
   a.ctx_out = e->ctx;
   a.ctx_bf16 = 1;
+  a.group_ws = e->group_ws;
   a.trace = nullptr;
   return a;
 }
 
 // Attention for one layer: one cluster launch over the whole batch.
-void enqueue_attention(kvp_engine* e, int l) { launch_layer(e->lplan, fused_args(e, l), e->stream); }
+void enqueue_attention(kvp_engine* e, int l) {
+  launch_layer(e->lplan, fused_args(e, l), e->stream);
+}
 
 // One decode step over all layers, enqueued on e->stream (graph-capturable).
 void enqueue_step(kvp_engine* e) {
@@ -233,12 +250,13 @@ __global__ void f32_to_bf16_kernel(const float* in, __nv_bfloat16* out, long n) 
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) out[i] = __float2bfloat16_rn(in[i]);
 }
-// fp32 row-major [rows][W] -> bf16 head-major [W/D][rows][D]
-__global__ void f32_to_bf16_heads_kernel(const float* in, __nv_bfloat16* out, int rows, int W, int D) {
+// fp32 row-major [rows][W] -> bf16 packed row tiles per kv head
+__global__ void f32_to_bf16_packed_kernel(const float* in, __nv_bfloat16* out, int rows, int W, int D) {
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= static_cast<long>(rows) * W) return;
-  const long r = i / W, c = i % W;
-  out[((c / D) * rows + r) * D + c % D] = __float2bfloat16_rn(in[i]);
+  const long r = i / W;
+  const int c = static_cast<int>(i % W);
+  out[packed_row_off(r, c, D, (rows + 127) / 128)] = __float2bfloat16_rn(in[i]);
 }
 
 // Visual prefill K/V of every instance of layer l, fp32 [2B][T][W] (K of b at 2b, V at 2b+1),
@@ -307,10 +325,10 @@ void compact_visual(kvp_engine* e) {
         const size_t m = static_cast<size_t>(b) * 2 + kind;
         __nv_bfloat16* rdst = (kind == 0 ? e->rkf + static_cast<size_t>(l) * e->right_k_elems()
                                          : e->rvf + static_cast<size_t>(l) * e->right_v_elems()) +
-                              static_cast<size_t>(b) * R * W;
+                              static_cast<size_t>(b) * e->Hkv * kvp_engine::tiles(R) * 128 * e->D;
         const long nr = static_cast<long>(R) * W;
         launch_1d(nr, [&](unsigned g, int t) {
-          f32_to_bf16_heads_kernel<<<g, t, 0, s>>>(right + m * R * W, rdst, R, W, e->D);
+          f32_to_bf16_packed_kernel<<<g, t, 0, s>>>(right + m * R * W, rdst, R, W, e->D);
         });
         const long nlft = static_cast<long>(T) * R;
         launch_1d(nlft, [&](unsigned g, int t) {
@@ -405,6 +423,9 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     e->xcur = e->alloc<float>(static_cast<size_t>(e->B) * e->HD);
     e->yout = e->alloc<float>(static_cast<size_t>(e->B) * e->HD);
     e->n_tail_dev = e->alloc<int>(1);
+    const size_t gws = layer_group_ws_bytes(e->lplan);
+    e->group_ws = e->alloc<unsigned char>(gws);
+    KVP_CUDA(cudaMemset(e->group_ws, 0, gws));
     *out = e.release();
   });
 }
@@ -441,7 +462,7 @@ extern "C" int kvp_engine_prefill(kvp_engine* e) {
         for (int b = 0; b < e->B; ++b)
           for (int kind = 0; kind < 2; ++kind) {
             __nv_bfloat16* dst = (kind == 0 ? e->tk : e->tv) + static_cast<size_t>(l) * e->tail_elems() +
-                                 static_cast<size_t>(b) * e->cap * e->W;
+                                 static_cast<size_t>(b) * e->Hkv * kvp_engine::tiles(e->cap) * 128 * e->D;
             const auto& pr = e->cfg.textual;
             launch_1d(static_cast<long>(e->t0) * e->W, [&](unsigned g, int t) {
               latent_direct_kernel<<<g, t, 0, s>>>(dst, e->cap, e->t0, e->Hkv, e->D, pr.true_rank,
@@ -464,7 +485,7 @@ extern "C" int kvp_engine_prefill(kvp_engine* e) {
           for (int b = 0; b < e->B; ++b) {
             __nv_bfloat16* right = (kind == 0 ? e->rkf + static_cast<size_t>(l) * e->right_k_elems()
                                               : e->rvf + static_cast<size_t>(l) * e->right_v_elems()) +
-                                   static_cast<size_t>(b) * rank * e->W;
+                                   static_cast<size_t>(b) * e->Hkv * kvp_engine::tiles(rank) * 128 * e->D;
             launch_1d(static_cast<long>(e->n) * rank + static_cast<long>(rank) * e->W, [&](unsigned g, int t) {
               synth_factor_kernel<<<g, t, 0, s>>>(scratch + static_cast<size_t>(b) * e->n * rank, e->n, rank, right,
                                                   e->W, e->D, seed, stream_id(2, b, l, kind));

@@ -71,9 +71,10 @@ def layer_state(eng, l):
     st = {"n_tail": v.n_tail}
     st["left_k"] = unpack_left(d2h(v.left_k, pk), s["B"], s["n"], s["rank"])
     st["left_v"] = unpack_left(d2h(v.left_v, pk), s["B"], s["n"], s["rank"])
-    def heads(ptr, rows):  # head-major [B][Hkv][rows][D] -> row-major [B][rows][W]
-        raw = bf16_to_f64(d2h(ptr, s["B"] * rows * W * 2).view(np.uint16))
-        return raw.reshape(s["B"], s["Hkv"], rows, s["D"]).transpose(0, 2, 1, 3).reshape(s["B"], rows, W)
+    def heads(ptr, rows):  # packed row tiles per kv head -> row-major [B][rows][W]
+        nb = capi.lib().kvp_packed_left_bytes(s["B"] * s["Hkv"], rows, s["D"])
+        hm = unpack_left(d2h(ptr, nb), s["B"] * s["Hkv"], rows, s["D"])
+        return hm.reshape(s["B"], s["Hkv"], rows, s["D"]).transpose(0, 2, 1, 3).reshape(s["B"], rows, W)
     st["right_k"] = heads(v.right_k, s["rank"])
     st["right_v"] = heads(v.right_v, s["rank"])
     st["tail_k"] = heads(v.tail_k, cap)

@@ -48,10 +48,11 @@ def main():
             out = torch.empty(capi.lib().kvp_packed_left_bytes(B, n, r), dtype=torch.uint8, device=dev)
             capi.call("kvp_pack_left", src.data_ptr(), r, B, n, r, out.data_ptr(), None)
             return out
-        L = dict(lk=packed(rk), lv=packed(rv),
-                 rk=(torch.randn(B, rk, W, device=dev) / W ** 0.5).to(bf),
-                 rv=(torch.randn(B, rv, W, device=dev) / W ** 0.5).to(bf),
-                 tk=torch.randn(B, cap, W, device=dev).to(bf), tv=torch.randn(B, cap, W, device=dev).to(bf),
+        def rows_packed(rows, sc):  # packed row tiles per kv head, random contents
+            nel = capi.lib().kvp_packed_left_bytes(B * Hkv, rows, D) // 2
+            return (torch.randn(nel, device=dev) * sc).to(bf)
+        L = dict(lk=packed(rk), lv=packed(rv), rk=rows_packed(rk, W ** -0.5), rv=rows_packed(rv, W ** -0.5),
+                 tk=rows_packed(cap, 1.0), tv=rows_packed(cap, 1.0),
                  q=torch.randn(B, H * D, device=dev), imp=torch.rand(B, n + cap, device=dev, dtype=torch.float64),
                  ctx=torch.empty(B, H * D, device=dev, dtype=bf))
         L["desc"] = FusedDesc(H, Hkv, D, B, n, rk, rv, 0, cap, nt, None, args.cluster, 1, L["lk"].data_ptr(),
@@ -92,11 +93,11 @@ def main():
                 r = it[k] - t00
                 rel = (it[k, 2] - it[k, 1]).item() if it[k, 2] > 0 else float("nan")
                 print(f"  {k:4d} {r[0].item():9.0f} {r[1].item():9.0f} {rel:7.0f}   {(r[1] - r[0]).item():7.0f}")
-        t = buf[:B * cl * 16].view(B * cl, 16)[:, :11].double().cpu()
+        t = buf[:B * cl * 16].view(B * cl, 16)[:, :15].double().cpu()
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
         names = ["start", "A pushed", "S ready", "p tiles", "U ready", "U reduced", "D done", "prod done",
-                 "mma P ok", "-", "-"]
+                 "mma P ok", "m_loc", "p tile 0", "EMA done", "U wait", "gathered", "tail EMA"]
         rel = (t - t0) / 1000.0
         print("phase (us since first CTA start): median / max over CTAs")
         for k, n_ in enumerate(names):
