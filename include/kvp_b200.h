@@ -151,20 +151,11 @@ int kvp_assign_groups_host(int32_t n, const double* scores, int32_t n_groups, co
 size_t kvp_packed_left_bytes(int32_t batch, int32_t n, int32_t rank);
 /* Row-major [batch][n][ld] bf16 left factor -> packed layout. */
 int kvp_pack_left(const void* src, int64_t ld, int32_t batch, int32_t n, int32_t rank, void* dst, void* stream);
-/* Right factors and dense tails are stored head-major: [batch][kv_heads][rows][head_dim]
- * bf16, so one kv head's slice (what one CTA streams) is contiguous.  Converts
- * from (to_heads = 1) or back to (to_heads = 0) the reference's row-major
- * Matrix layout [batch][rows][kv_heads*head_dim] (matrix.hpp:17-67).  src != dst. */
-int kvp_pack_heads(const void* src, void* dst, int32_t batch, int32_t rows, int32_t kv_heads, int32_t head_dim,
-                   int32_t to_heads, void* stream);
 
 /* One layer of a batch of caches in the serving layout: every instance holds
- * one factored block of n_comp tokens (left_k/left_v packed, see above) and a
- * dense tail.  right_k / right_v ([rank][kv_heads*head_dim] per instance) and
- * tail_k / tail_v ([tail_cap][kv_heads*head_dim]) are stored per kv head in the
- * same packed row-tile layout: kvp_pack_heads to head-major, then kvp_pack_left
- * with batch = batch*kv_heads, n = rows, rank = head_dim (head_dim 64 or 128).
- * n_tail rows of the tail are valid — read from
+ * one factored block of n_comp tokens (left_k/left_v packed, see above;
+ * right_k: [batch][rank_k][W], right_v: [batch][rank_v][W]) and a dense tail
+ * (tail_k/tail_v: [batch][tail_cap][W], n_tail rows valid — read from
  * n_tail_dev when non-NULL so the call can live in a CUDA graph).  This is
  * the plan build_retrieval_plan produces for the reference's default
  * configuration (visual block factored, textual tail dense; decoder.cpp:141-188)
@@ -194,15 +185,14 @@ typedef struct {
   size_t workspace_bytes;
 } kvp_fused_desc;
 
-/* Bytes of device workspace kvp_decode_fused needs for `desc`: 0 (the layer
- * kernel keeps P, U and the tail weights on chip); kept for ABI stability. */
+/* Bytes of device workspace kvp_decode_fused needs for `desc` (P, tail
+ * weights and U between its three launches); pass it to make the call
+ * allocation-free (and CUDA-graph capturable). */
 size_t kvp_decode_fused_workspace(const kvp_fused_desc* desc);
 
-/* decode_step's attention + importance for a whole batch (decoder.cpp:583-601)
- * in one launch: a thread-block cluster per instance projects q into the key
- * basis, scores the compressed coefficients and the tail on the tensor cores,
- * applies softmax and the EMA, accumulates softmax.V in the low-rank space and
- * does one value-basis multiply.  KVP_ERR_PARAMETER when the shape is outside the
+/* decode_step's attention + importance for a whole batch (decoder.cpp:583-601):
+ * qdots (project q into the key basis + tail logits), the cluster/tcgen05
+ * low-rank core, and vsum (value basis multiply + tail values) — 3 launches.  KVP_ERR_PARAMETER when the shape is outside the
  * fused kernel's envelope (then use kvp_attend_plan). */
 int kvp_decode_fused(const kvp_fused_desc* desc, void* stream);
 
@@ -235,7 +225,7 @@ typedef struct {
   uint64_t svd_seed;
   int32_t svd_oversampling, svd_power_iterations;
   int32_t factor_init;          /* 0: compaction of the generated K/V; 1: placeholder factors */
-  int32_t cluster;              /* CTAs per instance in the decode kernel, 0 = auto */
+  int32_t cluster;              /* CTAs per instance in the decode core, 0 = auto */
 } kvp_engine_config;
 
 typedef struct {
@@ -248,9 +238,7 @@ typedef struct {
   uint64_t importance_bytes_per_token; /* fp64 read + write per token, all layers/instances */
 } kvp_engine_info;
 
-/* Device pointers of one layer's state (for tests / inspection): left factors
- * packed (kvp_pack_left), right factors and tails in the packed row-tile layout
- * of kvp_decode_fused. */
+/* Device pointers of one layer's state (for tests / inspection). */
 typedef struct {
   const void *left_k, *left_v, *right_k, *right_v, *tail_k, *tail_v;
   const double* importance;

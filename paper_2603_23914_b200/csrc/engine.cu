@@ -26,7 +26,6 @@
 #include "decode_fused.cuh"
 #include "engine.cuh"
 #include "philox.cuh"
-#include "sm100.cuh"
 
 struct kvp_engine {
   kvp_engine_config cfg{};
@@ -42,8 +41,14 @@ struct kvp_engine {
   __nv_bfloat16 *xb = nullptr, *ctx = nullptr;
   float *qkv = nullptr, *q = nullptr, *xin = nullptr, *xcur = nullptr, *yout = nullptr;
   int* n_tail_dev = nullptr;
-  kvp::LayerPlan lplan{};  // one-launch layer kernel
-  unsigned char* group_ws = nullptr;  // its L2 exchange area (shared by the layers: launches serialise)
+  void* fused_ws = nullptr;
+  size_t fused_ws_bytes = 0;
+  kvp::FusedPlan plan{};   // whole batch (workspace, tensor maps)
+  kvp::FusedPlan gplan{};  // one instance group (launch grids)
+  int groups = 1;          // instance groups pipelined across two streams
+  int core_priority = 0;
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_q0 = nullptr, ev_join = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   double compaction_ms = 0.0;
@@ -63,16 +68,16 @@ struct kvp_engine {
     if (graph) cudaGraphDestroy(graph);
     for (void* p : allocations) cudaFree(p);
     if (blas) cublasDestroy(blas);
+    for (cudaEvent_t ev : {ev_fork, ev_q0, ev_join})
+      if (ev) cudaEventDestroy(ev);
+    if (stream2) cudaStreamDestroy(stream2);
     if (stream) cudaStreamDestroy(stream);
   }
   size_t lk_bytes() const { return kvp::packed_left_bytes(B, n, rk); }  // per layer, packed
   size_t lv_bytes() const { return kvp::packed_left_bytes(B, n, rv); }
-  // right factors and tails: packed 128-row tiles per kv head (kvp_pack_left layout of the
-  // head-major [B*Hkv][rows][D] matrices)
-  static size_t tiles(int rows) { return static_cast<size_t>((rows + 127) / 128); }
-  size_t right_k_elems() const { return static_cast<size_t>(B) * Hkv * tiles(rk) * 128 * D; }
-  size_t right_v_elems() const { return static_cast<size_t>(B) * Hkv * tiles(rv) * 128 * D; }
-  size_t tail_elems() const { return static_cast<size_t>(B) * Hkv * tiles(cap) * 128 * D; }
+  size_t right_k_elems() const { return static_cast<size_t>(B) * rk * W; }
+  size_t right_v_elems() const { return static_cast<size_t>(B) * rv * W; }
+  size_t tail_elems() const { return static_cast<size_t>(B) * cap * W; }
   size_t imp_stride() const { return static_cast<size_t>(n) + cap; }
 };
 
@@ -81,15 +86,6 @@ namespace {
 
 void blas_check(cublasStatus_t s, const char* what) {
   if (s != CUBLAS_STATUS_SUCCESS) fail(KVP_ERR_CUDA, std::string(what) + ": cuBLAS status " + std::to_string(s));
-}
-
-// Element offset of (row r, column c = g*D + d) of one instance's [rows][Hkv*D]
-// matrix in the packed row-tile layout: tile (g, r / 128), 64-column panel d / 64,
-// 128-byte row r % 128 with 16-byte chunks XOR-swizzled by the row (sm100::sw128_off).
-__device__ __forceinline__ long packed_row_off(long r, int c, int D, int tiles_per_head) {
-  const int g = c / D, d = c % D;
-  const long tile = static_cast<long>(g) * tiles_per_head + r / 128;
-  return (tile * (D / 64) + d / 64) * 8192 + kvp::sm100::sw128_off(static_cast<uint32_t>(r % 128), d % 64) / 2;
 }
 
 // W ~ N(0,1) / sqrt(HD) from the reference's weight streams (harness.cpp:138-151):
@@ -107,8 +103,7 @@ __global__ void gen_weight_kernel(__nv_bfloat16* out, long ld_out, int col0, int
 // consumed as z (T x r, latent i scaled by decay^i), shared loadings
 // (shared x D), per-head loadings (Hkv x (r - shared) x D), then noise (T x W).
 // out[t, h*D + j] = sum_i z[t,i] * load_h[i, j] + noise * g.
-// Written in the packed tail layout (rows_cap rows per kv head).
-__global__ void latent_direct_kernel(__nv_bfloat16* out, int rows_cap, int T, int Hkv, int D, int r, int shared,
+__global__ void latent_direct_kernel(__nv_bfloat16* out, long ld_out, int T, int Hkv, int D, int r, int shared,
                                      double decay, double noise, uint64_t seed, uint64_t stream) {
   const long idx = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int W = Hkv * D;
@@ -126,14 +121,14 @@ __global__ void latent_direct_kernel(__nv_bfloat16* out, int rows_cap, int T, in
     sc *= decay;
   }
   if (noise > 0.0) acc += noise * philox_gaussian(seed, stream, base_n + static_cast<uint64_t>(t) * W + col);
-  out[packed_row_off(t, col, D, (rows_cap + 127) / 128)] = __float2bfloat16_rn(static_cast<float>(acc));
+  out[static_cast<long>(t) * ld_out + col] = __float2bfloat16_rn(static_cast<float>(acc));
 }
 
 // Placeholder factors for factor_init = 1 (decode-only benchmarking): left
 // rows N(0,1) * 0.98^r (row-major scratch, packed afterwards), right rows
-// N(0,1)/sqrt(W) (near-orthonormal for W >> R), stored head-major.
-__global__ void synth_factor_kernel(__nv_bfloat16* left, int n, int rank, __nv_bfloat16* right, int W, int D,
-                                    uint64_t seed, uint64_t stream) {
+// N(0,1)/sqrt(W) (near-orthonormal for W >> R).
+__global__ void synth_factor_kernel(__nv_bfloat16* left, int n, int rank, __nv_bfloat16* right, int W, uint64_t seed,
+                                    uint64_t stream) {
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long nl = static_cast<long>(n) * rank, nr = static_cast<long>(rank) * W;
   if (i < nl) {
@@ -141,9 +136,7 @@ __global__ void synth_factor_kernel(__nv_bfloat16* left, int n, int rank, __nv_b
     left[i] = __float2bfloat16_rn(static_cast<float>(philox_gaussian(seed, stream, i) * pow(0.98, r)));
   } else if (i < nl + nr) {
     const long k = i - nl;
-    const long r = k / W, c = k % W;
-    right[packed_row_off(r, static_cast<int>(c), D, (rank + 127) / 128)] =
-        __float2bfloat16_rn(static_cast<float>(philox_gaussian(seed, stream ^ 0x5A5Aull, k)) * rsqrtf(float(W)));
+    right[k] = __float2bfloat16_rn(static_cast<float>(philox_gaussian(seed, stream ^ 0x5A5Aull, k)) * rsqrtf(float(W)));
   }
 }
 
@@ -153,6 +146,25 @@ __global__ void to_bf16_kernel(const float* in, __nv_bfloat16* out, long n) {
 }
 
 __global__ void bump_counter_kernel(int* c) { *c += 1; }
+
+// Split [q | k | v] (fp32, B x (HD + 2W)); q -> q buffer, k/v -> bf16 tail row
+// (n_tail - 1), new token importance 0 (cache.cpp:147-170, importance.cpp:9-14).
+__global__ void append_kernel(const float* qkv, float* q, __nv_bfloat16* tk, __nv_bfloat16* tv, double* imp,
+                              const int* n_tail, int HD, int W, int cap, int n_comp, long imp_stride) {
+  const int b = blockIdx.y;
+  const int row = *n_tail - 1;
+  const float* src = qkv + static_cast<long>(b) * (HD + 2 * W);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < HD + 2 * W; i += gridDim.x * blockDim.x) {
+    if (i < HD) {
+      q[static_cast<long>(b) * HD + i] = src[i];
+    } else if (i < HD + W) {
+      tk[(static_cast<long>(b) * cap + row) * W + (i - HD)] = __float2bfloat16_rn(src[i]);
+    } else {
+      tv[(static_cast<long>(b) * cap + row) * W + (i - HD - W)] = __float2bfloat16_rn(src[i]);
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) imp[static_cast<long>(b) * imp_stride + n_comp + row] = 0.0;
+}
 
 void launch_1d(long n, auto&& f) {
   const int threads = 256;
@@ -193,14 +205,42 @@ FusedArgs fused_args(kvp_engine* e, int l) {
   a.head_avg = nullptr;
   a.ctx_out = e->ctx;
   a.ctx_bf16 = 1;
-  a.group_ws = e->group_ws;
+  a.ws_pimg = static_cast<unsigned char*>(e->fused_ws);
+  a.ws_tail = reinterpret_cast<float*>(a.ws_pimg + static_cast<size_t>(e->B) * 2 * e->plan.kpk * e->plan.np * 128);
+  a.ws_u = a.ws_tail + static_cast<size_t>(e->B) * e->H * e->cap;
   a.trace = nullptr;
   return a;
 }
 
-// Attention for one layer: one cluster launch over the whole batch.
+// Attention for one layer, instance groups pipelined over two streams:
+// qdots(g0) -> [core(g0) || qdots(g1)] -> [vsum(g0) || core(g1)] -> vsum(g1).
 void enqueue_attention(kvp_engine* e, int l) {
-  launch_layer(e->lplan, fused_args(e, l), e->stream);
+  cudaStream_t s = e->stream;
+  const FusedArgs full = fused_args(e, l);
+  if (e->groups == 1) {
+    launch_qdots(e->gplan, full, s);
+    launch_core(e->gplan, full, s, e->core_priority);
+    launch_vsum(e->gplan, full, s);
+    return;
+  }
+  const int gb = e->gplan.s.batch;
+  KVP_CUDA(cudaEventRecord(e->ev_fork, s));
+  KVP_CUDA(cudaStreamWaitEvent(e->stream2, e->ev_fork, 0));
+  const FusedArgs a0 = offset_args(e->plan, full, 0);
+  launch_qdots(e->gplan, a0, s);
+  KVP_CUDA(cudaEventRecord(e->ev_q0, s));
+  launch_core(e->gplan, a0, s, e->core_priority);
+  launch_vsum(e->gplan, a0, s);
+  for (int g = 1; g < e->groups; ++g) {
+    const FusedArgs ag = offset_args(e->plan, full, g * gb);
+    KVP_CUDA(cudaStreamWaitEvent(e->stream2, e->ev_q0, 0));
+    launch_qdots(e->gplan, ag, e->stream2);
+    KVP_CUDA(cudaEventRecord(e->ev_q0, e->stream2));
+    launch_core(e->gplan, ag, e->stream2, e->core_priority);
+    launch_vsum(e->gplan, ag, e->stream2);
+  }
+  KVP_CUDA(cudaEventRecord(e->ev_join, e->stream2));
+  KVP_CUDA(cudaStreamWaitEvent(s, e->ev_join, 0));
 }
 
 // One decode step over all layers, enqueued on e->stream (graph-capturable).
@@ -250,14 +290,6 @@ __global__ void f32_to_bf16_kernel(const float* in, __nv_bfloat16* out, long n) 
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i < n) out[i] = __float2bfloat16_rn(in[i]);
 }
-// fp32 row-major [rows][W] -> bf16 packed row tiles per kv head
-__global__ void f32_to_bf16_packed_kernel(const float* in, __nv_bfloat16* out, int rows, int W, int D) {
-  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= static_cast<long>(rows) * W) return;
-  const long r = i / W;
-  const int c = static_cast<int>(i % W);
-  out[packed_row_off(r, c, D, (rows + 127) / 128)] = __float2bfloat16_rn(in[i]);
-}
 
 // Visual prefill K/V of every instance of layer l, fp32 [2B][T][W] (K of b at 2b, V at 2b+1),
 // from the latent-factor model with the reference's Philox streams.
@@ -297,7 +329,7 @@ void generate_visual(kvp_engine* e, int l, float* a, float* zbuf, float* lbuf) {
 
 // Prefill compaction (compress_now for the visual segment of every instance
 // and layer): generate K/V, randomized SVD, store bf16 factors in the decode
-// layout (left packed, right head-major).
+// layout (left packed, right row-major).
 void compact_visual(kvp_engine* e) {
   cudaStream_t s = e->stream;
   const int T = e->n, W = e->W;
@@ -325,11 +357,9 @@ void compact_visual(kvp_engine* e) {
         const size_t m = static_cast<size_t>(b) * 2 + kind;
         __nv_bfloat16* rdst = (kind == 0 ? e->rkf + static_cast<size_t>(l) * e->right_k_elems()
                                          : e->rvf + static_cast<size_t>(l) * e->right_v_elems()) +
-                              static_cast<size_t>(b) * e->Hkv * kvp_engine::tiles(R) * 128 * e->D;
+                              static_cast<size_t>(b) * R * W;
         const long nr = static_cast<long>(R) * W;
-        launch_1d(nr, [&](unsigned g, int t) {
-          f32_to_bf16_packed_kernel<<<g, t, 0, s>>>(right + m * R * W, rdst, R, W, e->D);
-        });
+        launch_1d(nr, [&](unsigned g, int t) { f32_to_bf16_kernel<<<g, t, 0, s>>>(right + m * R * W, rdst, nr); });
         const long nlft = static_cast<long>(T) * R;
         launch_1d(nlft, [&](unsigned g, int t) {
           f32_to_bf16_kernel<<<g, t, 0, s>>>(left + m * T * R, lb + static_cast<size_t>(b) * T * R, nlft);
@@ -396,10 +426,23 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     e->rv = std::min(c->rank_v, std::min(e->n, e->W));
     e->ld = 0;
     FusedShape fs{e->H, e->Hkv, e->D, e->n, e->rk, e->rv, e->ld, e->cap, e->B, c->cluster};
-    if (fs.cluster <= 0) fs.cluster = auto_layer_cluster(fs);
-    e->lplan = plan_layer(fs);
-    require(e->lplan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->lplan.why).c_str());
+    if (fs.cluster <= 0) fs.cluster = auto_cluster_size(fs);
+    e->plan = plan_fused(fs);
+    require(e->plan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->plan.why).c_str());
+    e->groups = 1;  // two-group pipelining measured slower on B200 (KVP_GROUPS to override)
+    if (const char* g = std::getenv("KVP_GROUPS")) e->groups = std::max(1, std::atoi(g));
+    require(e->B % e->groups == 0, KVP_ERR_PARAMETER, "engine: batch must divide into the instance groups");
+    FusedShape gs = fs;
+    gs.batch = e->B / e->groups;
+    e->gplan = plan_fused(gs);
+    require(e->gplan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->gplan.why).c_str());
+    int lo = 0, hi = 0;
+    KVP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    e->core_priority = hi;  // numerically lowest = highest priority
     KVP_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+    KVP_CUDA(cudaStreamCreateWithFlags(&e->stream2, cudaStreamNonBlocking));
+    for (cudaEvent_t* ev : {&e->ev_fork, &e->ev_q0, &e->ev_join})
+      KVP_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     blas_check(cublasCreate(&e->blas), "cublasCreate");
     blas_check(cublasSetStream(e->blas, e->stream), "cublasSetStream");
     const size_t blas_ws = 32u << 20;
@@ -423,9 +466,9 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     e->xcur = e->alloc<float>(static_cast<size_t>(e->B) * e->HD);
     e->yout = e->alloc<float>(static_cast<size_t>(e->B) * e->HD);
     e->n_tail_dev = e->alloc<int>(1);
-    const size_t gws = layer_group_ws_bytes(e->lplan);
-    e->group_ws = e->alloc<unsigned char>(gws);
-    KVP_CUDA(cudaMemset(e->group_ws, 0, gws));
+    e->fused_ws_bytes = fused_workspace_bytes(fs);
+    e->fused_ws = e->alloc<char>(e->fused_ws_bytes);
+    KVP_CUDA(cudaMemset(e->fused_ws, 0, e->fused_ws_bytes));
     *out = e.release();
   });
 }
@@ -462,10 +505,10 @@ extern "C" int kvp_engine_prefill(kvp_engine* e) {
         for (int b = 0; b < e->B; ++b)
           for (int kind = 0; kind < 2; ++kind) {
             __nv_bfloat16* dst = (kind == 0 ? e->tk : e->tv) + static_cast<size_t>(l) * e->tail_elems() +
-                                 static_cast<size_t>(b) * e->Hkv * kvp_engine::tiles(e->cap) * 128 * e->D;
+                                 static_cast<size_t>(b) * e->cap * e->W;
             const auto& pr = e->cfg.textual;
             launch_1d(static_cast<long>(e->t0) * e->W, [&](unsigned g, int t) {
-              latent_direct_kernel<<<g, t, 0, s>>>(dst, e->cap, e->t0, e->Hkv, e->D, pr.true_rank,
+              latent_direct_kernel<<<g, t, 0, s>>>(dst, e->W, e->t0, e->Hkv, e->D, pr.true_rank,
                                                    std::min(pr.shared_subspace, pr.true_rank), pr.spectrum_decay,
                                                    pr.noise_floor, seed, stream_id(2, b, l, 2 + kind));
             });
@@ -485,10 +528,10 @@ extern "C" int kvp_engine_prefill(kvp_engine* e) {
           for (int b = 0; b < e->B; ++b) {
             __nv_bfloat16* right = (kind == 0 ? e->rkf + static_cast<size_t>(l) * e->right_k_elems()
                                               : e->rvf + static_cast<size_t>(l) * e->right_v_elems()) +
-                                   static_cast<size_t>(b) * e->Hkv * kvp_engine::tiles(rank) * 128 * e->D;
+                                   static_cast<size_t>(b) * rank * e->W;
             launch_1d(static_cast<long>(e->n) * rank + static_cast<long>(rank) * e->W, [&](unsigned g, int t) {
               synth_factor_kernel<<<g, t, 0, s>>>(scratch + static_cast<size_t>(b) * e->n * rank, e->n, rank, right,
-                                                  e->W, e->D, seed, stream_id(2, b, l, kind));
+                                                  e->W, seed, stream_id(2, b, l, kind));
             });
           }
           unsigned char* dst = kind == 0 ? e->lk + static_cast<size_t>(l) * e->lk_bytes()
@@ -563,7 +606,7 @@ extern "C" int kvp_engine_get_info(kvp_engine* e, kvp_engine_info* info) {
   return guarded([&] {
     require(e && info, KVP_ERR_PARAMETER, "engine: null argument");
     std::memset(info, 0, sizeof(*info));
-    info->cluster = e->lplan.s.cluster;
+    info->cluster = e->plan.s.cluster;
     info->rank_k = e->rk;
     info->rank_v = e->rv;
     info->ld_left = e->ld;
@@ -627,7 +670,7 @@ extern "C" int kvp_engine_time_attention(kvp_engine* e, int32_t iters, double* m
     KVP_CUDA(cudaEventSynchronize(e1));
     float ms = 0.f;
     KVP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-    note_launch(static_cast<uint64_t>(iters + 1) * e->L);
+    note_launch(static_cast<uint64_t>(iters + 1) * e->L * 3);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     cudaGraphExecDestroy(ge);

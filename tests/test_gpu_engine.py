@@ -71,14 +71,12 @@ def layer_state(eng, l):
     st = {"n_tail": v.n_tail}
     st["left_k"] = unpack_left(d2h(v.left_k, pk), s["B"], s["n"], s["rank"])
     st["left_v"] = unpack_left(d2h(v.left_v, pk), s["B"], s["n"], s["rank"])
-    def heads(ptr, rows):  # packed row tiles per kv head -> row-major [B][rows][W]
-        nb = capi.lib().kvp_packed_left_bytes(s["B"] * s["Hkv"], rows, s["D"])
-        hm = unpack_left(d2h(ptr, nb), s["B"] * s["Hkv"], rows, s["D"])
-        return hm.reshape(s["B"], s["Hkv"], rows, s["D"]).transpose(0, 2, 1, 3).reshape(s["B"], rows, W)
-    st["right_k"] = heads(v.right_k, s["rank"])
-    st["right_v"] = heads(v.right_v, s["rank"])
-    st["tail_k"] = heads(v.tail_k, cap)
-    st["tail_v"] = heads(v.tail_v, cap)
+    nr = s["B"] * s["rank"] * W * 2
+    st["right_k"] = bf16_to_f64(d2h(v.right_k, nr).view(np.uint16)).reshape(s["B"], s["rank"], W)
+    st["right_v"] = bf16_to_f64(d2h(v.right_v, nr).view(np.uint16)).reshape(s["B"], s["rank"], W)
+    nt = s["B"] * cap * W * 2
+    st["tail_k"] = bf16_to_f64(d2h(v.tail_k, nt).view(np.uint16)).reshape(s["B"], cap, W)
+    st["tail_v"] = bf16_to_f64(d2h(v.tail_v, nt).view(np.uint16)).reshape(s["B"], cap, W)
     st["imp"] = d2h(v.importance, s["B"] * (s["n"] + cap) * 8).view(np.float64).reshape(s["B"], s["n"] + cap)
     st["wqkv"] = bf16_to_f64(d2h(v.w_qkv, HD * (HD + 2 * W) * 2).view(np.uint16)).reshape(HD, HD + 2 * W)
     st["wo"] = bf16_to_f64(d2h(v.w_o, HD * HD * 2).view(np.uint16)).reshape(HD, HD)

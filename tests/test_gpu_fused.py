@@ -79,20 +79,8 @@ def run_fused(case, H, Hkv, D, nt, alpha, cluster=0, ld_pad=8):
         capi.call("kvp_pack_left", src.data_ptr(), r, B, n, r, out.data_ptr(), None)
         return out
     bf = lambda x: torch.as_tensor(x).to(torch.bfloat16).cuda().contiguous()
-
-    def heads(x):  # row-major [B][rows][W] -> packed row tiles per kv head (serving layout)
-        src = bf(x)
-        hm = torch.empty_like(src)  # head-major [B][Hkv][rows][D] through kvp_pack_heads
-        capi.call("kvp_pack_heads", src.data_ptr(), hm.data_ptr(), B, x.shape[1], Hkv, D, 1, None)
-        back = torch.empty_like(src)
-        capi.call("kvp_pack_heads", hm.data_ptr(), back.data_ptr(), B, x.shape[1], Hkv, D, 0, None)
-        assert torch.equal(back, src)  # the inverse restores the reference's row-major Matrix
-        rows = x.shape[1]
-        out = torch.zeros(capi.lib().kvp_packed_left_bytes(B * Hkv, rows, D), dtype=torch.uint8, device="cuda")
-        capi.call("kvp_pack_left", hm.data_ptr(), D, B * Hkv, rows, D, out.data_ptr(), None)
-        return out
-    t = dict(lk=left(case["left_k"]), lv=left(case["left_v"]), rk=heads(case["right_k"]), rv=heads(case["right_v"]),
-             tk=heads(case["tail_k"]), tv=heads(case["tail_v"]), q=torch.as_tensor(case["q"], dtype=torch.float32).cuda(),
+    t = dict(lk=left(case["left_k"]), lv=left(case["left_v"]), rk=bf(case["right_k"]), rv=bf(case["right_v"]),
+             tk=bf(case["tail_k"]), tv=bf(case["tail_v"]), q=torch.as_tensor(case["q"], dtype=torch.float32).cuda(),
              imp=torch.as_tensor(case["imp"]).cuda().contiguous())
     ctx = torch.zeros((B, H * D), dtype=torch.float32, device="cuda")
     ha = torch.zeros((B, n + cap), dtype=torch.float32, device="cuda")

@@ -17,9 +17,6 @@ from paper_2603_23914_b200._capi import FusedDesc  # noqa: E402
 
 CONFIGS = {
     "c2": dict(B=16, H=32, Hkv=32, D=128, n=2304, rk=368, rv=368, nt=64 + 128, cap=320),
-    "c2b1": dict(B=1, H=32, Hkv=32, D=128, n=2304, rk=368, rv=368, nt=64 + 128, cap=320),
-    "c2b4": dict(B=4, H=32, Hkv=32, D=128, n=2304, rk=368, rv=368, nt=64 + 128, cap=320),
-    "c2r384": dict(B=16, H=32, Hkv=32, D=128, n=2304, rk=384, rv=384, nt=64 + 128, cap=320),
     "c3": dict(B=64, H=40, Hkv=40, D=128, n=4096, rk=284, rv=284, nt=64 + 128, cap=320),
     "c5": dict(B=32, H=32, Hkv=32, D=128, n=2048, rk=128, rv=128, nt=64 + 128, cap=320),
     "c4_8x": dict(B=16, H=32, Hkv=32, D=128, n=4096, rk=256, rv=256, nt=64 + 128, cap=320),
@@ -48,11 +45,10 @@ def main():
             out = torch.empty(capi.lib().kvp_packed_left_bytes(B, n, r), dtype=torch.uint8, device=dev)
             capi.call("kvp_pack_left", src.data_ptr(), r, B, n, r, out.data_ptr(), None)
             return out
-        def rows_packed(rows, sc):  # packed row tiles per kv head, random contents
-            nel = capi.lib().kvp_packed_left_bytes(B * Hkv, rows, D) // 2
-            return (torch.randn(nel, device=dev) * sc).to(bf)
-        L = dict(lk=packed(rk), lv=packed(rv), rk=rows_packed(rk, W ** -0.5), rv=rows_packed(rv, W ** -0.5),
-                 tk=rows_packed(cap, 1.0), tv=rows_packed(cap, 1.0),
+        L = dict(lk=packed(rk), lv=packed(rv),
+                 rk=(torch.randn(B, rk, W, device=dev) / W ** 0.5).to(bf),
+                 rv=(torch.randn(B, rv, W, device=dev) / W ** 0.5).to(bf),
+                 tk=torch.randn(B, cap, W, device=dev).to(bf), tv=torch.randn(B, cap, W, device=dev).to(bf),
                  q=torch.randn(B, H * D, device=dev), imp=torch.rand(B, n + cap, device=dev, dtype=torch.float64),
                  ctx=torch.empty(B, H * D, device=dev, dtype=bf))
         L["desc"] = FusedDesc(H, Hkv, D, B, n, rk, rv, 0, cap, nt, None, args.cluster, 1, L["lk"].data_ptr(),
@@ -74,30 +70,19 @@ def main():
     torch.cuda.synchronize()
     if args.trace:
         cl = args.cluster or 8  # trace buffer sized for the largest cluster
-        buf = torch.zeros(B * cl * 16 + 3 * 2048 + 2 * 2048, dtype=torch.int64, device=dev)
+        buf = torch.zeros(B * cl * 16, dtype=torch.int64, device=dev)
         capi.lib().kvp_debug_fused_trace.argtypes = [C.c_void_p]
         capi.lib().kvp_debug_fused_trace(buf.data_ptr())
         capi.check(fn(C.byref(layers[0]["desc"]), stream))
         torch.cuda.synchronize()
         capi.lib().kvp_debug_fused_trace(None)
         capi.lib().kvp_debug_fused_max_clusters.argtypes = [C.POINTER(FusedDesc)]
-        capi.lib().kvp_debug_fused_cluster.argtypes = [C.POINTER(FusedDesc)]
-        print("cluster", capi.lib().kvp_debug_fused_cluster(C.byref(layers[0]["desc"])), "max active clusters:",
-              capi.lib().kvp_debug_fused_max_clusters(C.byref(layers[0]["desc"])))
-        it = buf[B * cl * 16:B * cl * 16 + 3 * 512].view(-1, 3).double().cpu()
-        it = it[it[:, 0] > 0]
-        if it.shape[0]:
-            t00 = it[0, 0].item()
-            print("block 0 items (SM clocks since first issue): issue / acquire / release-acquire, acquire-issue")
-            for k in range(it.shape[0]):
-                r = it[k] - t00
-                rel = (it[k, 2] - it[k, 1]).item() if it[k, 2] > 0 else float("nan")
-                print(f"  {k:4d} {r[0].item():9.0f} {r[1].item():9.0f} {rel:7.0f}   {(r[1] - r[0]).item():7.0f}")
-        t = buf[:B * cl * 16].view(B * cl, 16)[:, :15].double().cpu()
+        print("max active clusters:", capi.lib().kvp_debug_fused_max_clusters(C.byref(layers[0]["desc"])))
+        t = buf.view(B * cl, 16)[:, :11].double().cpu()
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
-        names = ["start", "A pushed", "S ready", "p tiles", "U ready", "U reduced", "D done", "prod done",
-                 "mma P ok", "m_loc", "p tile 0", "EMA done", "U wait", "gathered", "tail EMA"]
+        names = ["start", "S ready", "local stats", "p tiles", "U ready", "end", "stats tmem", "stats bar",
+                 "mma P ok", "mma S done", "prod LV0"]
         rel = (t - t0) / 1000.0
         print("phase (us since first CTA start): median / max over CTAs")
         for k, n_ in enumerate(names):
