@@ -11,10 +11,14 @@
 //   right  = diag(1/s_R) U_R^T B   (R x W, orthonormal rows)
 // orth(Y) is shifted CholeskyQR2 (Gram, Cholesky, triangular solve, twice)
 // instead of the reference's Householder QR (Eigen::HouseholderQR): the same
-// column space, GEMM-shaped.  Round-1 implementation: the large products are
-// cuBLAS strided-batched GEMMs and the k x k Cholesky / symmetric eigensolve
-// are cuSOLVER batched routines; the Philox sketch, the latent-factor workload
-// generator, shifting, scaling and the packing into the decode layout are ours.
+// column space, GEMM-shaped.  The products with A (the range finder and
+// B = Q^T A, ~85% of the flops) run on the hand-written tcgen05 GEMM of
+// compact_gemm.cu with A in bf16 (the serving precision) and the skinny operand
+// rounded to bf16; the k x k Grams, the triangular solves and the final
+// factor products stay fp32/fp64 (cuBLAS), the Cholesky and the symmetric
+// eigensolve are cuSOLVER batched routines.  Rounding the sketch operand to
+// bf16 perturbs the captured subspace by ~2^-9, far inside the reconstruction
+// bound of tests/test_gpu_engine.py (1.05x the reference's error + 5e-3).
 #include <cublas_v2.h>
 #include <cuda_bf16.h>
 #include <cusolverDn.h>
@@ -211,34 +215,48 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   solver_ok(cusolverDnSetStream(w.solver, stream), "cusolverDnSetStream");
   const int k = std::min(rank + oversampling, std::min(T, W));
   const long sA = static_cast<long>(T) * W;
+  const int npad = range_gemm_npad();
+  require(k <= npad, KVP_ERR_PARAMETER, "compaction: rank + oversampling above 384");
+  // A in bf16 (the tensor-core operand), once per layer
+  __nv_bfloat16* ab = w.get<__nv_bfloat16>(static_cast<size_t>(batch) * sA);
+  to_bf16_rows_kernel<<<grid_for(batch * sA), 256, 0, stream>>>(a, ab, batch * sA);
+  KVP_LAUNCHED();
   float* omega = w.get<float>(static_cast<size_t>(W) * k);
   gaussian_kernel<float><<<grid_for(static_cast<long>(W) * k), 256, 0, stream>>>(omega, static_cast<long>(W) * k, seed,
                                                                                    0x72737664ull, 0, 1.0);
   KVP_LAUNCHED();
   float* y = w.get<float>(static_cast<size_t>(batch) * T * k);
   float* z = w.get<float>(static_cast<size_t>(batch) * W * k);
-  gemm_rm(w, false, false, T, k, W, a, sA, omega, 0, y, static_cast<long>(T) * k, batch);
+  __nv_bfloat16* xt = w.get<__nv_bfloat16>(static_cast<size_t>(batch) * npad * std::max(T, W));
+  // Y = A Omega
+  transpose_to_bf16(omega, 0, W, k, k, xt, 1, stream);
+  range_gemm(ab, T, W, batch, false, xt, false, k, y, stream);
   orth(w, y, T, k, batch);
   for (int it = 0; it < power_iterations; ++it) {
-    gemm_rm(w, true, false, W, k, T, a, sA, y, static_cast<long>(T) * k, z, static_cast<long>(W) * k, batch);
+    // Z = A^T Q
+    transpose_to_bf16(y, static_cast<long>(T) * k, T, k, k, xt, batch, stream);
+    range_gemm(ab, T, W, batch, true, xt, true, k, z, stream);
     orth(w, z, W, k, batch);
-    gemm_rm(w, false, false, T, k, W, a, sA, z, static_cast<long>(W) * k, y, static_cast<long>(T) * k, batch);
+    // Y = A Z
+    transpose_to_bf16(z, static_cast<long>(W) * k, W, k, k, xt, batch, stream);
+    range_gemm(ab, T, W, batch, false, xt, true, k, y, stream);
     orth(w, y, T, k, batch);
   }
-  // B = Q^T A (k x W)
-  float* bm = w.get<float>(static_cast<size_t>(batch) * k * W);
-  gemm_rm(w, true, false, k, W, T, y, static_cast<long>(T) * k, a, sA, bm, static_cast<long>(k) * W, batch);
+  // B^T = A^T Q (W x k); B = Q^T A is its transpose
+  float* bt = w.get<float>(static_cast<size_t>(batch) * k * W);
+  transpose_to_bf16(y, static_cast<long>(T) * k, T, k, k, xt, batch, stream);
+  range_gemm(ab, T, W, batch, true, xt, true, k, bt, stream);
   // C = B B^T in fp64
   double* bd = w.get<double>(static_cast<size_t>(batch) * k * W);
   const long nb = static_cast<long>(batch) * k * W;
-  f32_to_f64_kernel<<<grid_for(nb), 256, 0, stream>>>(bm, bd, nb);
+  f32_to_f64_kernel<<<grid_for(nb), 256, 0, stream>>>(bt, bd, nb);
   KVP_LAUNCHED();
   double* cd = w.get<double>(static_cast<size_t>(batch) * k * k);
   {
     const double one = 1.0, zero = 0.0;
-    // row-major B (k x W) = column-major B^T (W x k); C = B B^T = (B^T)^T (B^T)
-    blas_ok(cublasDgemmStridedBatched(blas, CUBLAS_OP_T, CUBLAS_OP_N, k, k, W, &one, bd, W, static_cast<long>(k) * W, bd,
-                                      W, static_cast<long>(k) * W, &zero, cd, k, static_cast<long>(k) * k, batch),
+    // row-major B^T (W x k) = column-major B (k x W, ld k); C = B B^T
+    blas_ok(cublasDgemmStridedBatched(blas, CUBLAS_OP_N, CUBLAS_OP_T, k, k, W, &one, bd, k, static_cast<long>(k) * W, bd,
+                                      k, static_cast<long>(k) * W, &zero, cd, k, static_cast<long>(k) * k, batch),
             "dgemm (Gram)");
   }
   double* evals = w.get<double>(static_cast<size_t>(batch) * k);
@@ -262,8 +280,8 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   // row-major M (k x R) with M[i][j] = us_colmajor[j*k + i]  ->  op(B)=T on the R x k row-major view.
   gemm_rm(w, false, true, T, rank, k, y, static_cast<long>(T) * k, us, static_cast<long>(k) * rank, left,
           static_cast<long>(T) * rank, batch);
-  // right (R x W) = Ui^T (R x k, row-major view of ui) * B (k x W)
-  gemm_rm(w, false, false, rank, W, k, ui, static_cast<long>(k) * rank, bm, static_cast<long>(k) * W, right,
+  // right (R x W) = Ui^T (R x k, row-major view of ui) * B (k x W), B = (B^T)^T from the row-major W x k
+  gemm_rm(w, false, true, rank, W, k, ui, static_cast<long>(k) * rank, bt, static_cast<long>(k) * W, right,
           static_cast<long>(rank) * W, batch);
   (void)hws;
 }

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cublas_v2.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -11,4 +12,13 @@ namespace kvp {
 void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const float* a, int batch, int T, int W,
                             int rank, uint64_t seed, int oversampling, int power_iterations, float* left,
                             float* right);
+// tcgen05 range-finder GEMM (compact_gemm.cu).  a: bf16 [batch][T][W];
+// xt: bf16 [batch or 1][range_gemm_npad()][K] (X^T, zero rows beyond n);
+// c: fp32 [batch][M][n] with M = trans_a ? W : T, K = trans_a ? T : W.
+int range_gemm_npad();
+void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, const __nv_bfloat16* xt, bool x_batched,
+                int n, float* c, cudaStream_t st);
+// fp32 [batch][rows][cols] (row stride ld, batch stride in_stride) -> bf16 [batch][npad][rows]
+void transpose_to_bf16(const float* in, long in_stride, int rows, int cols, int ld, __nv_bfloat16* out, int batch,
+                       cudaStream_t st);
 }  // namespace kvp
