@@ -110,14 +110,20 @@ class ClockSampler:
 
 
 def dist_setup():
+    """One process per GPU under torchrun: NCCL on a GPU box, gloo when no GPU is
+    visible (the multi-process CPU tests).  Only the barrier and the max-over-ranks
+    of the device-timed region use it: instances are sharded, no data-path collective."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
         import torch
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     return world, rank, local
 
 
@@ -132,9 +138,15 @@ def max_over_ranks(x, world):
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
+
+
+def aggregate_throughput(world, batch_per_rank, steps, ms):
+    """Whole-job tokens/s: every rank decodes its own instances (weak scaling)."""
+    return world * batch_per_rank * steps / (ms * 1e-3)
 
 
 def cpu_reference(cfg, steps, warmup, threads=None):
@@ -251,7 +263,7 @@ def main():
     ms = max_over_ranks(e0.elapsed_time(e1), world)
     tail_at = cfg["textual"] + args.warmup + 1
     config_block["tail_tokens_at_timing"] = [tail_at, tail_at + args.steps - 1]
-    value = world * B * args.steps / (ms * 1e-3)
+    value = aggregate_throughput(world, B, args.steps, ms)
 
     # ---- roofline: the attention launches alone at the final tail length
     att_ms, att_bytes = eng.time_attention(iters=3)

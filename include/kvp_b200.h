@@ -140,6 +140,21 @@ int kvp_assign_groups_host(int32_t n, const double* scores, int32_t n_groups, co
                            const int32_t* ranks, uint32_t* tier_out);
 
 /* ------------------------------------------------------------------------ */
+/* Truncated SVD (linalg.hpp:29-30 truncated_svd, linalg.cpp:68-105).         */
+/* ------------------------------------------------------------------------ */
+
+/* Rank-R factorisation of `batch` row-major fp32 matrices a[b] (T x W):
+ * left[b] (T x R, singular values folded in), right[b] (R x W, orthonormal
+ * rows), sv[b] (R singular values, descending; nullable).  method 1 =
+ * randomized (Halko: k = min(R + oversampling, min(T, W)), q power
+ * iterations, Philox sketch stream 0x72737664), range-finder products on the
+ * tcgen05 GEMM in bf16; method 0 = exact up to fp32 rounding (full sketch,
+ * fp32 products).  Errors as check_svd_input (linalg.cpp:15-24). */
+int kvp_truncated_svd(const float* a, int32_t batch, int32_t T, int32_t W, int32_t rank, int32_t method,
+                      uint64_t seed, int32_t oversampling, int32_t power_iterations, float* left, float* right,
+                      float* sv, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Fused serving kernel: bf16 compressed cache, T_q = 1, batched instances.  */
 /* ------------------------------------------------------------------------ */
 

@@ -198,7 +198,7 @@ void orth(SvdWork& w, float* y, int m, int k, int batch) {
 
 void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const float* a, int batch, int T, int W,
                             int rank, uint64_t seed, int oversampling, int power_iterations, float* left,
-                            float* right) {
+                            float* right, bool precise, float* sv) {
   // cuSOLVER handles are expensive to create: one per process, re-bound to the stream
   static cusolverDnHandle_t solver = nullptr;
   static cusolverDnParams_t params = nullptr;
@@ -216,36 +216,43 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   const int k = std::min(rank + oversampling, std::min(T, W));
   const long sA = static_cast<long>(T) * W;
   const int npad = range_gemm_npad();
-  require(k <= npad, KVP_ERR_PARAMETER, "compaction: rank + oversampling above 384");
-  // A in bf16 (the tensor-core operand), once per layer
-  __nv_bfloat16* ab = w.get<__nv_bfloat16>(static_cast<size_t>(batch) * sA);
-  to_bf16_rows_kernel<<<grid_for(batch * sA), 256, 0, stream>>>(a, ab, batch * sA);
-  KVP_LAUNCHED();
+  // the tcgen05 range finder (bf16 operands) unless fp32 products are asked for or the shape is outside it
+  const bool tc = !precise && k <= npad && T % 8 == 0 && W % 8 == 0;
+  __nv_bfloat16* ab = nullptr;
+  if (tc) {  // A in bf16 (the tensor-core operand), once per layer
+    ab = w.get<__nv_bfloat16>(static_cast<size_t>(batch) * sA);
+    to_bf16_rows_kernel<<<grid_for(batch * sA), 256, 0, stream>>>(a, ab, batch * sA);
+    KVP_LAUNCHED();
+  }
   float* omega = w.get<float>(static_cast<size_t>(W) * k);
   gaussian_kernel<float><<<grid_for(static_cast<long>(W) * k), 256, 0, stream>>>(omega, static_cast<long>(W) * k, seed,
                                                                                    0x72737664ull, 0, 1.0);
   KVP_LAUNCHED();
   float* y = w.get<float>(static_cast<size_t>(batch) * T * k);
   float* z = w.get<float>(static_cast<size_t>(batch) * W * k);
-  __nv_bfloat16* xt = w.get<__nv_bfloat16>(static_cast<size_t>(batch) * npad * std::max(T, W));
-  // Y = A Omega
-  transpose_to_bf16(omega, 0, W, k, k, xt, 1, stream);
-  range_gemm(ab, T, W, batch, false, xt, false, k, y, stream);
+  __nv_bfloat16* xt = tc ? w.get<__nv_bfloat16>(static_cast<size_t>(batch) * npad * std::max(T, W)) : nullptr;
+  // C = A X (x_rows = W) or A^T X (x_rows = T), X: fp32 [x_batched ? batch : 1][x_rows][k]
+  auto product = [&](bool trans, const float* x, bool x_batched, float* c) {
+    const int xr = trans ? T : W;
+    if (tc) {
+      transpose_to_bf16(x, static_cast<long>(xr) * k, xr, k, k, xt, x_batched ? batch : 1, stream);
+      range_gemm(ab, T, W, batch, trans, xt, x_batched, k, c, stream);
+    } else {
+      gemm_rm(w, trans, false, trans ? W : T, k, xr, a, sA, x, x_batched ? static_cast<long>(xr) * k : 0, c,
+              static_cast<long>(trans ? W : T) * k, batch);
+    }
+  };
+  product(false, omega, false, y);  // Y = A Omega
   orth(w, y, T, k, batch);
   for (int it = 0; it < power_iterations; ++it) {
-    // Z = A^T Q
-    transpose_to_bf16(y, static_cast<long>(T) * k, T, k, k, xt, batch, stream);
-    range_gemm(ab, T, W, batch, true, xt, true, k, z, stream);
+    product(true, y, true, z);  // Z = A^T Q
     orth(w, z, W, k, batch);
-    // Y = A Z
-    transpose_to_bf16(z, static_cast<long>(W) * k, W, k, k, xt, batch, stream);
-    range_gemm(ab, T, W, batch, false, xt, true, k, y, stream);
+    product(false, z, true, y);  // Y = A Z
     orth(w, y, T, k, batch);
   }
   // B^T = A^T Q (W x k); B = Q^T A is its transpose
   float* bt = w.get<float>(static_cast<size_t>(batch) * k * W);
-  transpose_to_bf16(y, static_cast<long>(T) * k, T, k, k, xt, batch, stream);
-  range_gemm(ab, T, W, batch, true, xt, true, k, bt, stream);
+  product(true, y, true, bt);
   // C = B B^T in fp64
   double* bd = w.get<double>(static_cast<size_t>(batch) * k * W);
   const long nb = static_cast<long>(batch) * k * W;
@@ -273,7 +280,7 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   // left = Q (U_R s), right = (U_R / s)^T B
   float* us = w.get<float>(static_cast<size_t>(batch) * k * rank);
   float* ui = w.get<float>(static_cast<size_t>(batch) * k * rank);
-  ritz_kernel<<<batch, 256, 0, stream>>>(cd, evals, k, rank, us, ui, nullptr);
+  ritz_kernel<<<batch, 256, 0, stream>>>(cd, evals, k, rank, us, ui, sv);
   KVP_LAUNCHED();
   // us/ui are column-major k x R == row-major R x k (rows = components).
   // left (T x R) = Q (T x k) * Us (k x R): Us row-major (k x R) is ui^T... build explicitly:
@@ -287,3 +294,31 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
 }
 
 }  // namespace kvp
+
+// ---------------------------------------------------------------------------
+// C-ABI: truncated SVD of a batch of row-major fp32 matrices on the device
+// (linalg.hpp:29-30 truncated_svd).  method 1 (randomized) follows
+// linalg.cpp:68-105 with the tcgen05 range finder; method 0 (exact) uses a full
+// sketch (k = min(T, W)) with fp32 products, exact up to fp32 rounding.
+// ---------------------------------------------------------------------------
+extern "C" int kvp_truncated_svd(const float* a, int32_t batch, int32_t T, int32_t W, int32_t rank, int32_t method,
+                                 uint64_t seed, int32_t oversampling, int32_t power_iterations, float* left,
+                                 float* right, float* sv, void* stream) {
+  return kvp::guarded([&] {
+    using namespace kvp;
+    require(a && left && right, KVP_ERR_PARAMETER, "truncated_svd: null buffer");
+    require(batch >= 1, KVP_ERR_PARAMETER, "truncated_svd: batch must be >= 1");
+    require(T >= 1 && W >= 1, KVP_ERR_SHAPE, "truncated_svd: matrix must be non-empty");
+    require(rank >= 1 && rank <= std::min(T, W), KVP_ERR_PARAMETER,
+            "truncated_svd: rank must be in [1, min(rows, cols)]");
+    require(method == 0 || method == 1, KVP_ERR_PARAMETER, "truncated_svd: method must be exact (0) or randomized (1)");
+    require(oversampling >= 0 && power_iterations >= 0, KVP_ERR_PARAMETER, "truncated_svd: bad randomized options");
+    static cublasHandle_t blas = nullptr;
+    if (!blas) blas_ok(cublasCreate(&blas), "cublasCreate");
+    cudaStream_t st = as_stream(stream);
+    blas_ok(cublasSetStream(blas, st), "cublasSetStream");
+    const bool exact = method == 0;
+    randomized_svd_batched(blas, st, a, batch, T, W, rank, seed, exact ? std::min(T, W) : oversampling,
+                           exact ? 2 : power_iterations, left, right, exact, sv);
+  });
+}

@@ -11,7 +11,7 @@ namespace kvp {
 // a: batch x (T x W) row-major fp32; left: batch x (T x rank), right: batch x (rank x W).
 void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const float* a, int batch, int T, int W,
                             int rank, uint64_t seed, int oversampling, int power_iterations, float* left,
-                            float* right);
+                            float* right, bool precise = false, float* sv = nullptr);
 // tcgen05 range-finder GEMM (compact_gemm.cu).  a: bf16 [batch][T][W];
 // xt: bf16 [batch or 1][range_gemm_npad()][K] (X^T, zero rows beyond n);
 // c: fp32 [batch][M][n] with M = trans_a ? W : T, K = trans_a ? T : W.

@@ -1,0 +1,99 @@
+"""The kvpack-compatible Python surface (paper_2603_23914_b200.kvpack), ported
+from the reference's binding smoke tests (proj/tests/python/test_smoke.py).
+Host accounting is exact; the factorisation runs in fp32 on the GPU, so the
+reference's 1e-10 bounds become fp32 bounds (1e-5 relative), stated per test."""
+import numpy as np
+import pytest
+
+from paper_2603_23914_b200 import kvpack
+
+
+def _gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def test_compression_ratio_closed_form():  # test_smoke.py:15-20
+    assert kvpack.compression_ratio(1000, 5120, 64) == pytest.approx(13.071895424836601, abs=1e-12)
+    assert kvpack.compression_ratio(16, 128, 8) == pytest.approx(16 * 128 / (16 * 8 + 8 * 128))
+    assert kvpack.compression_ratio(100, 64, 0) == 1.0
+    with pytest.raises(ValueError):
+        kvpack.compression_ratio(0, 64, 4)
+
+
+def test_flops_reduction_exact():  # test_smoke.py:23-26
+    flops, reduction = kvpack.partial_decompress_flops(1000, 5120, [0.1, 0.9], [64, 16])
+    assert flops == 212992000
+    assert abs(reduction - 0.675) <= 1e-15
+    with pytest.raises(ValueError):
+        kvpack.partial_decompress_flops(10, 10, [0.5], [4, 2])
+
+
+def test_truncated_svd_validation():  # linalg.cpp:15-24 (checked before any device work)
+    with pytest.raises(ValueError):
+        kvpack.truncated_svd(np.ones((4, 3)), 0)
+    with pytest.raises(ValueError):
+        kvpack.truncated_svd(np.ones((4, 3)), 4)
+    with pytest.raises(ValueError):
+        kvpack.truncated_svd(np.full((4, 3), np.nan), 2)
+    left, right = kvpack.truncated_svd(np.zeros((5, 4)), 2)  # zero matrix: coordinate rows
+    assert not left.any() and np.array_equal(right, np.eye(2, 4))
+
+
+@pytest.mark.gpu
+def test_truncated_svd_matches_numpy():  # test_smoke.py:29-39, fp32: 1e-5 relative
+    _gpu()
+    rng = np.random.default_rng(3)
+    a = rng.standard_normal((40, 24))
+    left, right = kvpack.truncated_svd(a, 6)
+    assert left.shape == (40, 6) and right.shape == (6, 24)
+    err = np.linalg.norm(a - left @ right)
+    u, s, vt = np.linalg.svd(a, full_matrices=False)
+    best = np.linalg.norm(a - (u[:, :6] * s[:6]) @ vt[:6])
+    assert abs(err - best) <= 1e-5 * np.linalg.norm(a)
+    assert np.allclose(right @ right.T, np.eye(6), atol=1e-5)
+
+
+@pytest.mark.gpu
+def test_randomized_svd_close_to_optimal():  # test_smoke.py:42-50
+    _gpu()
+    rng = np.random.default_rng(4)
+    base = rng.standard_normal((60, 8)) @ rng.standard_normal((8, 30))
+    noisy = base + 0.01 * rng.standard_normal((60, 30))
+    left, right = kvpack.truncated_svd(noisy, 8, method="randomized", seed=1)
+    err = np.linalg.norm(noisy - left @ right)
+    s = np.linalg.svd(noisy, compute_uv=False)
+    best = float(np.sqrt((s[8:] ** 2).sum()))
+    assert err <= 1.5 * best
+
+
+@pytest.mark.gpu
+def test_variance_helpers():  # test_smoke.py:53-62, fp32 singular values
+    _gpu()
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((50, 10)) @ np.diag([8.0, 4.0, 2.0, 1.0, 0, 0, 0, 0, 0, 0])
+    s = np.linalg.svd(a, compute_uv=False)
+    assert np.allclose(kvpack.singular_values(a)[:4], s[:4], rtol=1e-5)
+    evr = kvpack.explained_variance_ratio(a, 2)
+    assert evr == pytest.approx(float((s[:2] ** 2).sum() / (s ** 2).sum()), abs=1e-6)
+    rank, achieved = kvpack.rank_for_variance(a, 0.999, 10)
+    assert achieved >= 0.999
+    assert kvpack.explained_variance_ratio(a, rank - 1) < 0.999
+
+
+@pytest.mark.gpu
+def test_ema_update_hand_case():  # test_smoke.py:65-69 (bit-exact EMA)
+    _gpu()
+    scores = kvpack.ema_update(np.array([0.4, 0.0]), np.array([[0.1, 0.9], [0.1, 0.9]]), alpha=0.25)
+    assert scores[0] == pytest.approx(0.11875, abs=1e-15)
+
+
+@pytest.mark.gpu
+def test_assign_groups_partition():  # test_smoke.py:72-81
+    _gpu()
+    masks = kvpack.assign_groups(np.array([0.9, 0.1, 0.2, 0.3, 0.4, 0.5, 0.6, 0.7, 0.05, 0.8]), [0.3, 0.3, 0.4],
+                                 [16, 8, 4])
+    assert [len(m) for m in masks] == [3, 3, 4]
+    assert sorted(i for m in masks for i in m) == list(range(10))
+    assert 0 in masks[0] and 8 in masks[2]

@@ -1,0 +1,51 @@
+"""The N > 1 plumbing of bench.py on CPU: world size 2 over gloo (127.0.0.1).
+Instances are sharded across ranks with no data-path collective (SURVEY.md
+§8e); the only collectives are the barrier and the max over ranks of the
+device-timed region, and `value` aggregates every rank's tokens."""
+import os
+import socket
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(RANK=str(rank), LOCAL_RANK=str(rank), WORLD_SIZE=str(world), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port), CUDA_VISIBLE_DEVICES="")
+    sys.path.insert(0, str(ROOT))
+    import bench
+    import torch.distributed as dist
+    w, r, _ = bench.dist_setup()
+    bench.barrier(w)
+    ms = bench.max_over_ranks(10.0 + r, w)  # rank 1 is the slower one
+    value = bench.aggregate_throughput(w, 16, 20, ms)
+    q.put((r, w, dist.get_backend(), ms, value))
+    dist.destroy_process_group()
+
+
+def test_two_rank_max_over_ranks_and_weak_scaling():
+    mp = pytest.importorskip("torch.multiprocessing")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [o[0] for o in out] == [0, 1]
+    for r, w, backend, ms, value in out:
+        assert (w, backend) == (2, "gloo")
+        assert ms == 11.0  # max over ranks, identical on every rank
+        assert value == pytest.approx(2 * 16 * 20 / 11e-3)
