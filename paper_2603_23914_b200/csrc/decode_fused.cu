@@ -60,7 +60,7 @@ constexpr int kTailMax = 96;
 constexpr int kStreamThreads = 256;  // qdots / vsum blocks
 constexpr int kStreamWarps = kStreamThreads / 32;
 #ifndef QD_UNROLL
-#define QD_UNROLL 2
+#define QD_UNROLL 1
 #endif
 
 struct Smem {
