@@ -165,6 +165,24 @@ def cpu_reference(cfg, steps, warmup, threads=None):
     return value, threads, desc, pair_s
 
 
+def warm_libraries(cfg):
+    """One same-shape randomized SVD through kvp_truncated_svd before the
+    engine's timed prefill, so the cuBLAS/cuSOLVER modules are paged in and
+    loaded outside the compaction timing (a fresh box otherwise pays that on
+    the first layer)."""
+    import torch
+    from paper_2603_23914_b200 import _capi
+
+    H, Hkv, D = cfg["geom"]
+    T, W, R = cfg["visual"], Hkv * D, cfg["rank"]
+    a = torch.randn((2, T, W), device="cuda", dtype=torch.float32)
+    left = torch.empty((2, T, R), device="cuda", dtype=torch.float32)
+    right = torch.empty((2, R, W), device="cuda", dtype=torch.float32)
+    _capi.call("kvp_truncated_svd", a.data_ptr(), 2, T, W, R, 1, 7, 8, 2, left.data_ptr(), right.data_ptr(),
+               None, None)
+    torch.cuda.synchronize()
+
+
 def compaction_block(cfg, info, world):
     """Prefill compaction against the tensor roofline: algorithmic flops
     2*T*W*k*(2q+2) per matrix, 2 matrices per (instance, layer)."""
@@ -183,7 +201,7 @@ def compaction_block(cfg, info, world):
             "sketch": k, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak if peak else None, "peak_source": src,
             "note": "randomized SVD + packing of every (instance, layer, K|V) visual segment, CUDA events; "
-                    "the synthetic K/V generation is excluded; first layer includes one-time library setup"}
+                    "the synthetic K/V generation is excluded; cuBLAS/cuSOLVER warmed by one same-shape SVD beforehand"}
 
 
 def main():
@@ -231,6 +249,8 @@ def main():
                       decode_steps=max(cfg["steps"], total_steps), rank_k=cfg["rank"], rank_v=cfg["rank"],
                       visual=ProfileSpec(2 * cfg["rank"], cfg["rank"], 0.98, 1e-2), seed=rank,
                       factor_init=args.factor_init)
+    if args.factor_init == "compaction":
+        warm_libraries(cfg)
     eng = Engine(spec)
     eng.prefill()
     info = eng.info()

@@ -57,7 +57,10 @@ constexpr int kComputeThreads = 512;
 constexpr int kComputeWarps = 16;
 constexpr uint32_t kBarCompute = 1;  // named barrier id for the compute warps
 constexpr int kTailMax = 96;
-constexpr int kStreamThreads = 256;  // qdots / vsum blocks
+#ifndef KVP_STREAM_THREADS
+#define KVP_STREAM_THREADS 256
+#endif
+constexpr int kStreamThreads = KVP_STREAM_THREADS;  // qdots / vsum blocks
 constexpr int kStreamWarps = kStreamThreads / 32;
 #ifndef QD_UNROLL
 #define QD_UNROLL 1
@@ -220,6 +223,8 @@ __global__ void __launch_bounds__(kStreamThreads) qdots_kernel(const FusedPlan p
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / LPH, gl = lane % LPH;
   const int H = p.s.H, W = p.s.Hkv * D;
+  griddep_wait();               // q (and the new k, v) come from the projection GEMM
+  griddep_launch_dependents();  // core may start its q-independent prologue and left_k stream
   const int n_tail = a.n_tail_dev ? *a.n_tail_dev : a.n_tail;
   const int rk = p.s.rank_k, rows = rk + n_tail;
   const float scale = rsqrtf(static_cast<float>(D));
@@ -359,28 +364,37 @@ __global__ void __launch_bounds__(kStreamThreads) vsum_kernel(const FusedPlan p,
   float* wts = vsm;
   const int wstride = (rv + p.s.tail_cap + 3) & ~3;
   float* red = vsm + PER_KV * wstride;
+  const __nv_bfloat16* rvb = a.right_v + static_cast<long>(b) * rv * W + g * D + col8;
+  const __nv_bfloat16* tvb = a.tail_v + static_cast<long>(b) * p.s.tail_cap * W + g * D + col8;
+  constexpr int U = 8;
+  const int stride = kStreamWarps * RPI;
+  uint4 raw[U];
+  auto issue = [&](int r0) {  // clamped, unconditional loads: all stay in flight
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = min(r0 + u * stride, rows - 1);
+      raw[u] = ldg_stream(r < rv ? rvb + static_cast<long>(r) * W : tvb + static_cast<long>(r - rv) * W);
+    }
+  };
+  int r0 = warp * RPI + rsub;
+  // The value basis and the tail (appended by qdots, which completed before core
+  // triggered this launch) do not depend on core: the first batch is in flight
+  // while core finishes.  The weights U / p_tail are core's output.
+  issue(r0);
+  griddep_wait();
   for (int i = threadIdx.x; i < PER_KV * rows; i += kStreamThreads) {
     const int y = i / rows, r = i % rows, h = g * PER_KV + y;
     wts[y * wstride + r] = r < rv ? a.ws_u[(static_cast<long>(b) * H + h) * rv + r]
                                   : a.ws_tail[(static_cast<long>(b) * H + h) * p.s.tail_cap + (r - rv)];
   }
   __syncthreads();
-  const __nv_bfloat16* rvb = a.right_v + static_cast<long>(b) * rv * W + g * D + col8;
-  const __nv_bfloat16* tvb = a.tail_v + static_cast<long>(b) * p.s.tail_cap * W + g * D + col8;
   float acc[PER_KV][8];
 #pragma unroll
   for (int y = 0; y < PER_KV; ++y)
 #pragma unroll
     for (int e = 0; e < 8; ++e) acc[y][e] = 0.f;
-  constexpr int U = 8;
-  const int stride = kStreamWarps * RPI;
-  for (int r0 = warp * RPI + rsub; r0 < rows; r0 += U * stride) {
-    uint4 raw[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {  // clamped, unconditional loads: all stay in flight
-      const int r = min(r0 + u * stride, rows - 1);
-      raw[u] = ldg_stream(r < rv ? rvb + static_cast<long>(r) * W : tvb + static_cast<long>(r - rv) * W);
-    }
+  for (; r0 < rows; r0 += U * stride) {
+    if (r0 != warp * RPI + rsub) issue(r0);
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int r = r0 + u * stride;
@@ -486,16 +500,31 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
+  // Programmatic dependent launch: everything above and the first ring of left_k
+  // stages is independent of qdots; qdots' outputs (P image, tail logits, the
+  // appended tail row's zeroed importance) are read only after griddep_wait.
+  const bool defer_wait = warp == 0 && lane == 0;
+  if (!defer_wait) {
+    griddep_wait();
+    griddep_launch_dependents();
+  }
   if (warp == 0) {
     // ===================== producer: left_k / left_v panels =====================
     if (lane == 0) {
-      {  // P operand image (bf16 hi/lo, already swizzled by qdots) -> smem in one bulk copy
+      auto load_p = [&] {  // P operand image (bf16 hi/lo, already swizzled by qdots) -> smem in one bulk copy
+        griddep_wait();
+        griddep_launch_dependents();
         const uint32_t pbytes = 2u * p.kpk * NP * 128;
         mbar_expect_tx(&bars[kPopReady], pbytes);
         bulk_load(smem + L.phi, reinterpret_cast<const unsigned char*>(a.ws_pimg) + static_cast<size_t>(b) * pbytes,
                   pbytes, &bars[kPopReady]);
-      }
+      };
+      bool p_loaded = false;
       for (int i = 0; i < it.total; ++i) {
+        if (i == NS) {  // the ring is full: the MMAs that free it need P
+          load_p();
+          p_loaded = true;
+        }
         const int s = i % NS;
         mbar_wait(&bars[kEmpty + s], ((i / NS) & 1) ^ 1);
         unsigned char* dst = smem + L.ring + s * kRing;
@@ -515,6 +544,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(full, bytes);
         bulk_load(dst, src, bytes, full);
       }
+      if (!p_loaded) load_p();
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
@@ -879,21 +909,45 @@ size_t fused_workspace_bytes(const FusedShape& s) {
   return static_cast<size_t>(s.batch) * (pimg + sizeof(float) * s.H * (static_cast<size_t>(s.tail_cap) + s.rank_v));
 }
 
+// Programmatic dependent launch of the three decode kernels (each waits with
+// griddepcontrol.wait before reading its predecessor's output).  KVP_PDL=0 turns it off.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("KVP_PDL");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+int pdl_attr(cudaLaunchAttribute& at) {
+  if (!pdl_enabled()) return 0;
+  at.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at.val.programmaticStreamSerializationAllowed = 1;
+  return 1;
+}
+
 template <int PER_KV, int D>
 void launch_stream_pair(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, bool first) {
   const dim3 grid(static_cast<unsigned>(p.s.Hkv), static_cast<unsigned>(p.s.batch));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(kStreamThreads);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_attr(attr[0]);
   if (first) {
-    qdots_kernel<PER_KV, D><<<grid, kStreamThreads, 0, st>>>(p, a);
+    KVP_CUDA(cudaLaunchKernelEx(&cfg, qdots_kernel<PER_KV, D>, p, a));
     KVP_LAUNCHED();
   } else {
     const size_t smem = (static_cast<size_t>(PER_KV) * ((p.s.rank_v + p.s.tail_cap + 3) & ~3) + kStreamWarps * (256 / D) * PER_KV * D) * 4;
-    static size_t attr = 0;
-    if (attr < smem) {
+    static size_t smem_attr = 0;
+    if (smem_attr < smem) {
       KVP_CUDA(cudaFuncSetAttribute(vsum_kernel<PER_KV, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(smem)));
-      attr = smem;
+      smem_attr = smem;
     }
-    vsum_kernel<PER_KV, D><<<grid, kStreamThreads, smem, st>>>(p, a);
+    cfg.dynamicSmemBytes = smem;
+    KVP_CUDA(cudaLaunchKernelEx(&cfg, vsum_kernel<PER_KV, D>, p, a));
     KVP_LAUNCHED();
   }
 }
@@ -956,15 +1010,19 @@ void launch_core(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, int pr
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = p.smem_bytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = static_cast<unsigned>(p.s.cluster);
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributePriority;
-  attr[1].val.priority = priority;
+  int na = 1;
+  if (priority != 0) {
+    attr[na].id = cudaLaunchAttributePriority;
+    attr[na++].val.priority = priority;
+  }
+  na += pdl_attr(attr[na]);
   cfg.attrs = attr;
-  cfg.numAttrs = priority != 0 ? 2 : 1;
+  cfg.numAttrs = static_cast<unsigned>(na);
   KVP_CUDA(cudaLaunchKernelEx(&cfg, kernel, p, a));
   KVP_LAUNCHED();
 }
