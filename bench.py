@@ -53,8 +53,9 @@ def load_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d.get("hbm_gbs", 6650.0)), "measured"
-    return 6650.0, "fallback"
+        if d.get("hbm_gbs"):
+            return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    return 6650.0, "fallback (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
 
 
 class ClockSampler:
@@ -324,7 +325,7 @@ def main():
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
                              "kernel": "decode attention (qdots + cluster core + vsum) per layer",
-                             "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_src})",
+                             "peak_source": peak_src,
                              "ms_per_layer": att_ms, "algorithmic_bytes_per_layer": att_bytes},
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": B * HD * 4,

@@ -23,6 +23,8 @@
 #include <cuda_bf16.h>
 #include <cusolverDn.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <string>
@@ -105,9 +107,24 @@ __global__ void ritz_kernel(const double* evec, const double* eval, int k, int R
   }
 }
 
-__global__ void to_bf16_rows_kernel(const float* in, __nv_bfloat16* out, long n) {
+// Column-major identity matrices, n = batch * k * k elements.
+__global__ void identity_kernel(double* m, int k, long n) {
   const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = __float2bfloat16_rn(in[i]);
+  if (i < n) {
+    const long e = i % (static_cast<long>(k) * k);
+    m[i] = (e / k == e % k) ? 1.0 : 0.0;
+  }
+}
+
+// hi = bf16(x) and (optionally) lo = bf16(x - hi)
+__global__ void to_bf16_rows_kernel(const float* in, __nv_bfloat16* out, __nv_bfloat16* lo, long n) {
+  const long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) {
+    const float x = in[i];
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    out[i] = h;
+    if (lo) lo[i] = __float2bfloat16_rn(x - __bfloat162float(h));
+  }
 }
 
 unsigned grid_for(long n) { return static_cast<unsigned>((n + 255) / 256); }
@@ -140,6 +157,10 @@ struct SvdWork {
 
 namespace {
 
+// fp32 products stay CUBLAS_COMPUTE_32F: the process shares torch's bundled
+// cuBLAS (12.8), which has no BF16x9 emulation.
+constexpr cublasComputeType_t kCompaction32F = CUBLAS_COMPUTE_32F;
+
 // Row-major C (m x n) = op(A) op(B), batched with strides (elements).
 void gemm_rm(SvdWork& w, bool ta, bool tb, int m, int n, int k, const float* a, long sa, const float* b, long sb,
              float* c, long sc, int batch) {
@@ -148,49 +169,52 @@ void gemm_rm(SvdWork& w, bool ta, bool tb, int m, int n, int k, const float* a, 
   const int lda = ta ? m : k, ldb = tb ? k : n;
   blas_ok(cublasGemmStridedBatchedEx(w.blas, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, n, m, k,
                                      &one, b, CUDA_R_32F, ldb, sb, a, CUDA_R_32F, lda, sa, &zero, c, CUDA_R_32F, n,
-                                     sc, batch, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
+                                     sc, batch, kCompaction32F, CUBLAS_GEMM_DEFAULT),
           "gemm (compaction)");
 }
 
-// Orthonormal basis of the columns of Y (m x k row-major, batch) in place:
-// shifted CholeskyQR2.  Row-major Y (m x k) is column-major Y^T (k x m).
-void orth(SvdWork& w, float* y, int m, int k, int batch) {
-  float* g = w.get<float>(static_cast<size_t>(batch) * k * k);
-  double* gd = w.get<double>(static_cast<size_t>(batch) * k * k);
-  std::vector<double*> gp(batch);
-  std::vector<float*> yp(batch);
-  double** d_gp = w.get<double*>(batch);
-  float** d_yp = w.get<float*>(batch);
-  float* gf = w.get<float>(static_cast<size_t>(batch) * k * k);
-  int* info = w.get<int>(batch);
+// Orthonormal basis of the columns of Y (m x k row-major, batch): shifted
+// CholeskyQR, `passes` times.  Row-major Y (m x k) is column-major Y^T (k x m).
+// Q = Y L^-T is one GEMM against the explicit inverse of the (fp64) Cholesky
+// factor, written to `spare`; the two buffers are swapped.
+void orth(SvdWork& w, float*& y, float*& spare, int m, int k, int batch, int passes) {
+  const long nk = static_cast<long>(batch) * k * k;
+  float* g = w.get<float>(nk);
+  double* gd = w.get<double>(nk);
+  double* linv = w.get<double>(nk);
+  float* linvf = w.get<float>(nk);
+  std::vector<double*> gp(batch), lp(batch);
   for (int i = 0; i < batch; ++i) {
     gp[i] = gd + static_cast<size_t>(i) * k * k;
-    yp[i] = y + static_cast<size_t>(i) * m * k;
+    lp[i] = linv + static_cast<size_t>(i) * k * k;
   }
+  double** d_gp = w.get<double*>(batch);
+  double** d_lp = w.get<double*>(batch);
+  int* info = w.get<int>(batch);
   KVP_CUDA(cudaMemcpyAsync(d_gp, gp.data(), sizeof(double*) * batch, cudaMemcpyHostToDevice, w.stream));
-  std::vector<float*> gfp(batch);
-  for (int i = 0; i < batch; ++i) gfp[i] = gf + static_cast<size_t>(i) * k * k;
-  float** d_gfp = w.get<float*>(batch);
-  KVP_CUDA(cudaMemcpyAsync(d_gfp, gfp.data(), sizeof(float*) * batch, cudaMemcpyHostToDevice, w.stream));
-  KVP_CUDA(cudaMemcpyAsync(d_yp, yp.data(), sizeof(float*) * batch, cudaMemcpyHostToDevice, w.stream));
-  for (int pass = 0; pass < 2; ++pass) {
+  KVP_CUDA(cudaMemcpyAsync(d_lp, lp.data(), sizeof(double*) * batch, cudaMemcpyHostToDevice, w.stream));
+  for (int pass = 0; pass < passes; ++pass) {
     // G = Y^T Y (k x k, symmetric; row/column-major identical)
     gemm_rm(w, true, false, k, k, m, y, static_cast<long>(m) * k, y, static_cast<long>(m) * k, g,
             static_cast<long>(k) * k, batch);
-    const long nk = static_cast<long>(batch) * k * k;
     f32_to_f64_kernel<<<grid_for(nk), 256, 0, w.stream>>>(g, gd, nk);
     KVP_LAUNCHED();
     shift_diag_kernel<<<batch, 256, 0, w.stream>>>(gd, k, pass == 0 ? 1e-5 : 1e-7);
     KVP_LAUNCHED();
-    // G = L L^T (column-major lower)
+    // G = L L^T (column-major lower), then L^-1 from L X = I in fp64
     solver_ok(cusolverDnDpotrfBatched(w.solver, CUBLAS_FILL_MODE_LOWER, k, d_gp, k, info, batch), "potrfBatched");
-    f64_to_f32_kernel<<<grid_for(nk), 256, 0, w.stream>>>(gd, gf, nk);
+    identity_kernel<<<grid_for(nk), 256, 0, w.stream>>>(linv, k, nk);
     KVP_LAUNCHED();
-    // Row-major Y L^-T  <=>  column-major (Y^T) solved as  L X = Y^T  (left, lower, no transpose)
-    const float one = 1.f;
-    blas_ok(cublasStrsmBatched(w.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k,
-                               m, &one, d_gfp, k, d_yp, k, batch),
-            "trsmBatched");
+    const double one = 1.0;
+    blas_ok(cublasDtrsmBatched(w.blas, CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, CUBLAS_DIAG_NON_UNIT, k,
+                               k, &one, d_gp, k, d_lp, k, batch),
+            "trsmBatched (L^-1)");
+    f64_to_f32_kernel<<<grid_for(nk), 256, 0, w.stream>>>(linv, linvf, nk);
+    KVP_LAUNCHED();
+    // column-major L^-1 read row-major is L^-T:  Q = Y L^-T
+    gemm_rm(w, false, false, m, k, k, y, static_cast<long>(m) * k, linvf, static_cast<long>(k) * k, spare,
+            static_cast<long>(m) * k, batch);
+    std::swap(y, spare);
   }
 }
 
@@ -206,6 +230,15 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
     solver_ok(cusolverDnCreate(&solver), "cusolverDnCreate");
     solver_ok(cusolverDnCreateParams(&params), "cusolverDnCreateParams");
   }
+  {  // the per-call workspace comes from the stream-ordered pool: keep its pages mapped
+     // between calls instead of returning them at every synchronisation
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   SvdWork w;
   w.blas = blas;
   w.stream = stream;
@@ -217,11 +250,19 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   const long sA = static_cast<long>(T) * W;
   const int npad = range_gemm_npad();
   // the tcgen05 range finder (bf16 operands) unless fp32 products are asked for or the shape is outside it
-  const bool tc = !precise && k <= npad && T % 8 == 0 && W % 8 == 0;
-  __nv_bfloat16* ab = nullptr;
-  if (tc) {  // A in bf16 (the tensor-core operand), once per layer
+  // diagnostics: KVP_SVD_FP32=1 forces the fp32 products, KVP_SVD_PASSES=2 two CholeskyQR passes everywhere
+  const bool force_fp32 = std::getenv("KVP_SVD_FP32") != nullptr;
+  const int min_passes = std::getenv("KVP_SVD_PASSES") ? std::atoi(std::getenv("KVP_SVD_PASSES")) : 1;
+  const bool tc = !precise && !force_fp32 && k <= npad && T % 8 == 0 && W % 8 == 0;
+  // The range finder only needs the subspace, so its products take bf16 operands.
+  // The last power-iteration product and B = Q^T A carry the factor values: they
+  // use the hi/lo split (KVP_SVD_SPLIT=0 turns it off, for comparison).
+  const bool split = tc && !(std::getenv("KVP_SVD_SPLIT") && std::atoi(std::getenv("KVP_SVD_SPLIT")) == 0);
+  __nv_bfloat16 *ab = nullptr, *ab_lo = nullptr;
+  if (tc) {  // A as bf16 hi (+ lo), the tensor-core operands, once per layer
     ab = w.get<__nv_bfloat16>(static_cast<size_t>(batch) * sA);
-    to_bf16_rows_kernel<<<grid_for(batch * sA), 256, 0, stream>>>(a, ab, batch * sA);
+    if (split) ab_lo = w.get<__nv_bfloat16>(static_cast<size_t>(batch) * sA);
+    to_bf16_rows_kernel<<<grid_for(batch * sA), 256, 0, stream>>>(a, ab, ab_lo, batch * sA);
     KVP_LAUNCHED();
   }
   float* omega = w.get<float>(static_cast<size_t>(W) * k);
@@ -230,29 +271,40 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   KVP_LAUNCHED();
   float* y = w.get<float>(static_cast<size_t>(batch) * T * k);
   float* z = w.get<float>(static_cast<size_t>(batch) * W * k);
+  float* y_spare = w.get<float>(static_cast<size_t>(batch) * T * k);
+  float* z_spare = w.get<float>(static_cast<size_t>(batch) * W * k);
   __nv_bfloat16* xt = tc ? w.get<__nv_bfloat16>(static_cast<size_t>(batch) * npad * std::max(T, W)) : nullptr;
   // C = A X (x_rows = W) or A^T X (x_rows = T), X: fp32 [x_batched ? batch : 1][x_rows][k]
-  auto product = [&](bool trans, const float* x, bool x_batched, float* c) {
+  // split: three-term hi/lo product (A_hi X_hi + A_hi X_lo + A_lo X_hi, ~2^-16 relative)
+  __nv_bfloat16* xt_lo = split ? w.get<__nv_bfloat16>(static_cast<size_t>(batch) * npad * std::max(T, W)) : nullptr;
+  auto product = [&](bool trans, const float* x, bool x_batched, float* c, bool three) {
     const int xr = trans ? T : W;
     if (tc) {
       transpose_to_bf16(x, static_cast<long>(xr) * k, xr, k, k, xt, x_batched ? batch : 1, stream);
       range_gemm(ab, T, W, batch, trans, xt, x_batched, k, c, stream);
+      if (three) {
+        transpose_to_bf16(x, static_cast<long>(xr) * k, xr, k, k, xt_lo, x_batched ? batch : 1, stream, true);
+        range_gemm(ab, T, W, batch, trans, xt_lo, x_batched, k, c, stream, true);
+        range_gemm(ab_lo, T, W, batch, trans, xt, x_batched, k, c, stream, true);
+      }
     } else {
       gemm_rm(w, trans, false, trans ? W : T, k, xr, a, sA, x, x_batched ? static_cast<long>(xr) * k : 0, c,
               static_cast<long>(trans ? W : T) * k, batch);
     }
   };
-  product(false, omega, false, y);  // Y = A Omega
-  orth(w, y, T, k, batch);
+  // Intermediate bases only need to be well conditioned with the right span (the
+  // next product re-mixes them), so one shifted CholeskyQR pass; the final Q gets two.
+  product(false, omega, false, y, false);  // Y = A Omega
+  orth(w, y, y_spare, T, k, batch, power_iterations > 0 ? min_passes : 2);
   for (int it = 0; it < power_iterations; ++it) {
-    product(true, y, true, z);  // Z = A^T Q
-    orth(w, z, W, k, batch);
-    product(false, z, true, y);  // Y = A Z
-    orth(w, y, T, k, batch);
+    product(true, y, true, z, false);  // Z = A^T Q
+    orth(w, z, z_spare, W, k, batch, min_passes);
+    product(false, z, true, y, split && it + 1 == power_iterations);  // Y = A Z
+    orth(w, y, y_spare, T, k, batch, it + 1 == power_iterations ? 2 : min_passes);
   }
   // B^T = A^T Q (W x k); B = Q^T A is its transpose
   float* bt = w.get<float>(static_cast<size_t>(batch) * k * W);
-  product(true, y, true, bt);
+  product(true, y, true, bt, split);
   // C = B B^T in fp64
   double* bd = w.get<double>(static_cast<size_t>(batch) * k * W);
   const long nb = static_cast<long>(batch) * k * W;

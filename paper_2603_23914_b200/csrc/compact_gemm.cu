@@ -43,7 +43,7 @@ constexpr uint32_t kGSmem = kGStages * kGStage + 1024;
 template <bool TRANS_A>
 __global__ void __launch_bounds__(kGThreads, 1)
     range_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_x, int M,
-                      int K, int n, int x_batched, float* __restrict__ c, long c_stride) {
+                      int K, int n, int x_batched, float* __restrict__ c, long c_stride, int accumulate) {
   extern __shared__ __align__(1024) unsigned char gsmem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsmem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[kGStages], empty[kGStages], done;
@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
       float v[8];
       tmem_ld8(tmem + (static_cast<uint32_t>(qd * 32) << 16) + static_cast<uint32_t>(c0), v);
       if (row < M) {
+        if (accumulate)
+          for (int e = 0; e < 8 && c0 + e < n; ++e) v[e] += crow[c0 + e];
         if (c0 + 8 <= n && (n & 3) == 0) {
           *reinterpret_cast<float4*>(crow + c0) = make_float4(v[0], v[1], v[2], v[3]);
           *reinterpret_cast<float4*>(crow + c0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
@@ -173,8 +175,9 @@ CUtensorMap encode_bf16(const void* base, int cols, int rows, int batch, int box
 
 // fp32 [batch][rows][cols] (row stride ld) -> bf16 [batch][cols_pad][rows]: the
 // transposed, K-major X operand; rows c >= cols are zero.
+// lo: the residual bf16(x - bf16(x)) instead of bf16(x) (second term of a hi/lo split).
 __global__ void transpose_bf16_kernel(const float* __restrict__ in, long in_stride, int rows, int cols, int ld,
-                                      __nv_bfloat16* __restrict__ out, int cols_pad) {
+                                      __nv_bfloat16* __restrict__ out, int cols_pad, int lo) {
   __shared__ float tile[32][33];
   const int b = blockIdx.z;
   const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
@@ -187,7 +190,11 @@ __global__ void transpose_bf16_kernel(const float* __restrict__ in, long in_stri
   __nv_bfloat16* dst = out + static_cast<long>(b) * cols_pad * rows;
   for (int i = threadIdx.y; i < 32; i += 8) {
     const int cc = c0 + i, r = r0 + threadIdx.x;
-    if (cc < cols_pad && r < rows) dst[static_cast<long>(cc) * rows + r] = __float2bfloat16_rn(tile[threadIdx.x][i]);
+    if (cc < cols_pad && r < rows) {
+      const float x = tile[threadIdx.x][i];
+      const __nv_bfloat16 h = __float2bfloat16_rn(x);
+      dst[static_cast<long>(cc) * rows + r] = lo ? __float2bfloat16_rn(x - __bfloat162float(h)) : h;
+    }
   }
 }
 
@@ -196,14 +203,14 @@ __global__ void transpose_bf16_kernel(const float* __restrict__ in, long in_stri
 int range_gemm_npad() { return kNPad; }
 
 void transpose_to_bf16(const float* in, long in_stride, int rows, int cols, int ld, __nv_bfloat16* out, int batch,
-                       cudaStream_t st) {
+                       cudaStream_t st, bool lo) {
   const dim3 grid((rows + 31) / 32, (kNPad + 31) / 32, batch);
-  transpose_bf16_kernel<<<grid, dim3(32, 8), 0, st>>>(in, in_stride, rows, cols, ld, out, kNPad);
+  transpose_bf16_kernel<<<grid, dim3(32, 8), 0, st>>>(in, in_stride, rows, cols, ld, out, kNPad, lo ? 1 : 0);
   KVP_LAUNCHED();
 }
 
 void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, const __nv_bfloat16* xt,
-                bool x_batched, int n, float* c, cudaStream_t st) {
+                bool x_batched, int n, float* c, cudaStream_t st, bool accumulate) {
   require(n <= kNPad, KVP_ERR_PARAMETER, "compaction: sketch width above 384 (rank + oversampling)");
   require(T % 8 == 0 && W % 8 == 0, KVP_ERR_PARAMETER, "compaction GEMM: T and W must be multiples of 8");
   const int M = trans_a ? W : T, K = trans_a ? T : W;
@@ -217,7 +224,8 @@ void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, c
     attr_set[trans_a] = true;
   }
   const dim3 grid((M + 127) / 128, batch);
-  kernel<<<grid, kGThreads, kGSmem, st>>>(ma, mx, M, K, n, x_batched ? 1 : 0, c, static_cast<long>(M) * n);
+  kernel<<<grid, kGThreads, kGSmem, st>>>(ma, mx, M, K, n, x_batched ? 1 : 0, c, static_cast<long>(M) * n,
+                                          accumulate ? 1 : 0);
   KVP_LAUNCHED();
 }
 

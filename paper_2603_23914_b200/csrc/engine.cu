@@ -388,6 +388,12 @@ void compact_visual(kvp_engine* e) {
   for (void* p : {static_cast<void*>(a), static_cast<void*>(zbuf), static_cast<void*>(lbuf), static_cast<void*>(left),
                   static_cast<void*>(right), static_cast<void*>(lb)})
     KVP_CUDA(cudaFreeAsync(p, s));
+  // prefill staging goes back to the device (the pool keeps pages mapped during compaction)
+  KVP_CUDA(cudaStreamSynchronize(s));
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+    cudaMemPoolTrimTo(pool, 0);
 }
 
 namespace {
