@@ -69,6 +69,25 @@ def test_randomized_svd_close_to_optimal():  # test_smoke.py:42-50
 
 
 @pytest.mark.gpu
+def test_randomized_svd_tracks_reference_at_tensor_core_shape():
+    # The tensor-core range finder (bf16 operands, hi/lo split for the last power
+    # iteration and B = Q^T A) against the reference's own randomized SVD
+    # (oracle/_ref, linalg.cpp:68-105) on a latent-factor matrix of the bench's
+    # kind: reconstruction error within 3% of the reference's, orthonormal rows.
+    _gpu()
+    from oracle import kvpack_oracle as ko
+    from oracle import ref
+    T, H, D, R = 1152, 16, 128, 184
+    a = ko.latent_factor_matrix(T, H, D, 2 * R, 0.98, R, 1e-2, 21, ko.stream_id(2, 0, 0, 0))
+    left, right = kvpack.truncated_svd(a, R, method="randomized", seed=0)
+    err = np.linalg.norm(a - left @ right) / np.linalg.norm(a)
+    rl, rr = ref.truncated_svd(a, R, method="randomized", seed=0)
+    ref_err = np.linalg.norm(a - rl @ rr) / np.linalg.norm(a)
+    assert err <= 1.03 * ref_err, (err, ref_err)
+    assert np.abs(right @ right.T - np.eye(R)).max() <= 1e-5
+
+
+@pytest.mark.gpu
 def test_variance_helpers():  # test_smoke.py:53-62, fp32 singular values
     _gpu()
     rng = np.random.default_rng(5)
