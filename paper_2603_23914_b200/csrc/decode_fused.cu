@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(kStreamThreads) qdots_kernel(const FusedPlan p
     __syncthreads();
   }
   const int NP = p.np;
-  const bool st = NP <= 32;
+  const bool st = p.stack;
   const uint32_t plane = static_cast<uint32_t>(p.kpk) * NP * 128;  // bytes of one (hi or lo) operand
   unsigned char* pimg = a.ws_pimg + static_cast<size_t>(b) * 2 * plane;
   float* tout = a.ws_tail + static_cast<long>(b) * H * p.s.tail_cap;
@@ -432,10 +432,9 @@ __global__ void __launch_bounds__(kStreamThreads) vsum_kernel(const FusedPlan p,
 // ============================================================================
 // 2. core: one cluster of C CTAs per instance.
 // ============================================================================
-template <int NPT>
+template <int NPT, bool ST>  // ST: hi/lo stacked along N (plan.stack)
 __global__ void __launch_bounds__(kThreads, 1)
     core_kernel(const FusedPlan p, const FusedArgs a) {
-  constexpr bool ST = NPT <= 32;               // hi/lo stacked along N
   constexpr int NPW = ST ? 2 * NPT : NPT;      // TMEM columns of one S / U tile
   extern __shared__ __align__(1024) unsigned char smem[];
   const Smem L = smem_layout(p);
@@ -877,8 +876,14 @@ FusedPlan plan_fused(const FusedShape& s) {
   p.tail_max = (s.tail_cap + s.cluster - 1) / s.cluster;
   if (p.tail_max > kTailMax) return bad("too many tail tokens per CTA (raise the cluster size)");
   p.heads_per_cta = (s.H + s.cluster - 1) / s.cluster;
-  const int npw = p.np <= 32 ? 2 * p.np : p.np;  // hi/lo stacked along N (core_kernel ST)
-  const int cols = p.max_tiles * npw + p.mtiles * npw;
+  // hi/lo stacked along N (one MMA per A panel) when the doubled tiles fit TMEM;
+  // otherwise two MMAs per K step into one tile (e.g. rank 1024)
+  p.stack = p.np <= 32;
+  int cols = p.max_tiles * (p.stack ? 2 * p.np : p.np) + p.mtiles * (p.stack ? 2 * p.np : p.np);
+  if (cols > 512 && p.stack) {
+    p.stack = false;
+    cols = p.max_tiles * p.np + p.mtiles * p.np;
+  }
   if (cols > 512) return bad("TMEM budget exceeded (raise the cluster size)");
   p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   p.stages = 2;
@@ -966,12 +971,12 @@ void launch_stream(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, bool
 }
 
 using CoreFn = void (*)(const FusedPlan, const FusedArgs);
-CoreFn core_for(int np) {
+CoreFn core_for(int np, bool stack) {
   switch (np) {
-    case 16: return core_kernel<16>;
-    case 32: return core_kernel<32>;
-    case 48: return core_kernel<48>;
-    default: return core_kernel<64>;
+    case 16: return stack ? core_kernel<16, true> : core_kernel<16, false>;
+    case 32: return stack ? core_kernel<32, true> : core_kernel<32, false>;
+    case 48: return core_kernel<48, false>;
+    default: return core_kernel<64, false>;
   }
 }
 
@@ -1003,7 +1008,7 @@ int prefetch_clusters(const FusedPlan& p) {
 }
 
 void launch_core(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, int priority) {
-  auto kernel = core_for(p.np);
+  auto kernel = core_for(p.np, p.stack);
   KVP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_bytes)));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>((p.s.batch + prefetch_clusters(p)) * p.s.cluster));
@@ -1065,7 +1070,7 @@ int max_active_clusters(const FusedPlan& p) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  auto kernel = core_for(p.np);
+  auto kernel = core_for(p.np, p.stack);
   KVP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_bytes)));
   int n = 0;
   KVP_CUDA(cudaOccupancyMaxActiveClusters(&n, kernel, &cfg));

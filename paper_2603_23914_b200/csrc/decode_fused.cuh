@@ -59,6 +59,7 @@ struct FusedPlan {
   int vpanels;         // V panels, even
   int mtiles;          // vpanels / 2
   int kst;             // ring stages per tile for left_k (panel pairs)
+  bool stack;          // P / p hi+lo halves stacked along N (np <= 32 and TMEM allows)
   int ntiles;          // 128-token tiles per instance
   int vpanels_st;      // stored V panels (ceil(rank_v / 64))
   int chunk;           // compressed tokens per CTA (max_tiles * 128)
