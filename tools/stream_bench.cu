@@ -193,7 +193,13 @@ int main(int argc, char** argv) {
     const int sb = argc > 12 ? atoi(argv[12]) : kStage;
     const long cta_stride = argc > 13 ? atol(argv[13]) : 0;
     const long per_run = argc > 14 ? atol(argv[14]) : per;
-    auto launch = [&] { cudaLaunchKernelEx(&cfg, k, map, (const char*)buf, per_run, stages, sink, panels, gap, variant, sb, cta_stride); };
+    // ROTATE=1: every launch reads a different region (inputs never L2-resident)
+    const bool rotate = getenv("ROTATE") != nullptr;
+    int rot = 0;
+    auto launch = [&] {
+      const char* base = (const char*)buf + (rotate ? static_cast<long>(rot++ % 7) * ctas * per_run : 0);
+      cudaLaunchKernelEx(&cfg, k, map, base, per_run, stages, sink, panels, gap, variant, sb, cta_stride);
+    };
     for (int rep = 0; rep < 2; ++rep) launch();
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
