@@ -62,6 +62,11 @@ constexpr int kTailMax = 96;
 #endif
 constexpr int kStreamThreads = KVP_STREAM_THREADS;  // qdots / vsum blocks
 constexpr int kStreamWarps = kStreamThreads / 32;
+// 4 resident blocks per SM (<= 64 registers): 512 (slice, instance) blocks fit one wave of 592 slots
+#ifndef KVP_STREAM_MINB
+#define KVP_STREAM_MINB 4
+#endif
+constexpr int kStreamMinBlocks = KVP_STREAM_MINB;
 #ifndef QD_UNROLL
 #define QD_UNROLL 1
 #endif
@@ -211,7 +216,7 @@ __device__ __forceinline__ void tld4_hilo(uint32_t taddr, int n, float (&v)[4]) 
 //    span one row segment and reduce with shuffles.
 // ============================================================================
 template <int PER_KV, int D>
-__global__ void __launch_bounds__(kStreamThreads) qdots_kernel(const FusedPlan p, const FusedArgs a) {
+__global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) qdots_kernel(const FusedPlan p, const FusedArgs a) {
   // A group of LPH = D/8 lanes covers one row segment (D bf16, one kv-head
   // slice); each lane owns one 16-byte chunk and keeps its 8 query values in
   // registers.  A group walks blocks of 8 consecutive rows: 8 independent
@@ -351,7 +356,7 @@ __global__ void __launch_bounds__(kStreamThreads) qdots_kernel(const FusedPlan p
 // 3. vsum: out[h, :] = sum_r U[h, r] right_v[r, g-slice] + sum_t p_tail[h, t] tail_v[t, g-slice]
 // ============================================================================
 template <int PER_KV, int D>
-__global__ void __launch_bounds__(kStreamThreads) vsum_kernel(const FusedPlan p, const FusedArgs a) {
+__global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) vsum_kernel(const FusedPlan p, const FusedArgs a) {
   constexpr int LPH = D / 8, RPI = 32 / LPH, NPART = kStreamWarps * RPI;
   extern __shared__ __align__(16) float vsm[];
   const int g = blockIdx.x, b = blockIdx.y;
