@@ -84,11 +84,24 @@ class ClockSampler:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 3:
                 try:
-                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16), time.monotonic()))
                 except ValueError:
                     pass
 
+    def wait_first(self, timeout=5.0):
+        """Block until nvidia-smi delivers its first sample (it needs ~0.1-0.5 s to start),
+        so that the timed region that follows is covered."""
+        end = time.monotonic() + timeout
+        while self.proc and not self.samples and time.monotonic() < end:
+            time.sleep(0.01)
+        self.t_begin = time.monotonic()
+
     def stop(self):
+        # one more sample after the timed region (100 ms period), so a short region is bracketed
+        t_end = time.monotonic()
+        end = t_end + 0.5
+        while self.proc and not any(x[3] >= t_end for x in self.samples) and time.monotonic() < end:
+            time.sleep(0.01)
         if self.proc:
             self.proc.terminate()
             try:
@@ -101,9 +114,14 @@ class ClockSampler:
                  0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        t0 = getattr(self, "t_begin", 0.0)
+        # the samples that bracket the timed region: from the last one before it through the first one after
+        before = [x for x in self.samples if x[3] < t0]
+        window = ([before[-1]] if before else []) + [x for x in self.samples if x[3] >= t0]
+        self.samples = window or self.samples
         sm = sorted(s[0] for s in self.samples)
         reasons = set()
-        for _, _, r in self.samples:
+        for _, _, r, _ in self.samples:
             for bit, n in names.items():
                 if r & bit and n != "gpu_idle":
                     reasons.add(n)
@@ -268,10 +286,11 @@ def main():
     # ---- device-resident timing
     run_steps(0, args.warmup)
     torch.cuda.synchronize()
-    barrier(world)
-    torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
+    sampler.wait_first()
+    barrier(world)
+    torch.cuda.synchronize()
     launches0 = _capi.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)

@@ -49,3 +49,20 @@ def test_two_rank_max_over_ranks_and_weak_scaling():
         assert (w, backend) == (2, "gloo")
         assert ms == 11.0  # max over ranks, identical on every rank
         assert value == pytest.approx(2 * 16 * 20 / 11e-3)
+
+
+def test_clock_sampler_window_and_reasons():
+    # bench.ClockSampler keeps the samples that bracket the timed region and
+    # reports the median SM clock and the throttle reasons seen there.
+    import time
+
+    import bench
+
+    s = bench.ClockSampler(0)
+    now = time.monotonic()
+    s.samples = [(1000.0, 1965.0, 0x0, now - 1.0), (1900.0, 1965.0, 0x0, now - 0.05),
+                 (1965.0, 1965.0, 0x4, now + 0.05), (1950.0, 1965.0, 0x0, now + 0.15)]
+    s.t_begin = now
+    out = s.stop()
+    assert out["sm_mhz"] == 1950.0 and out["sm_max_mhz"] == 1965.0
+    assert out["reasons"] == ["sw_power_cap"]
