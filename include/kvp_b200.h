@@ -174,12 +174,15 @@ int kvp_pack_left(const void* src, int64_t ld, int32_t batch, int32_t n, int32_t
  * n_tail_dev when non-NULL so the call can live in a CUDA graph).  This is
  * the plan build_retrieval_plan produces for the reference's default
  * configuration (visual block factored, textual tail dense; decoder.cpp:141-188)
- * with untiered decompression.  Outputs the pre-W_o context (decoder.cpp:587-590)
+ * with untiered decompression, or two-tier value decompression (key fractions 1;
+ * tier2_value_rank / value_tier).  Outputs the pre-W_o context (decoder.cpp:587-590)
  * and, when `importance` is set, applies the Eq. 1 EMA in place for T_q = 1
  * (importance.cpp:33-65) over [compressed..., tail...] columns. */
 typedef struct {
   int32_t heads, kv_heads, head_dim, batch;
-  int32_t n_comp, rank_k, rank_v, reserved;
+  int32_t n_comp, rank_k, rank_v;
+  int32_t tier2_value_rank;     /* attention-aware decompression (decoder.cpp:105-188): tokens flagged in
+                                   value_tier use only this prefix of the value rank; 0 = untiered */
   int32_t tail_cap, n_tail;
   const int32_t* n_tail_dev;    /* [dev] nullable */
   int32_t cluster;              /* CTAs per instance, 0 = auto */
@@ -198,6 +201,8 @@ typedef struct {
   void* context;                /* [dev] batch x H*D */
   void* workspace;              /* [dev] nullable: kvp_decode_fused_workspace() bytes */
   size_t workspace_bytes;
+  const uint8_t* value_tier;    /* [dev] batch x n_comp, nonzero = second tier (the group assign_groups puts
+                                   after the first ratio, importance.cpp:67-117); read when tier2_value_rank > 0 */
 } kvp_fused_desc;
 
 /* Bytes of device workspace kvp_decode_fused needs for `desc` (P, tail

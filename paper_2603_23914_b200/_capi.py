@@ -68,14 +68,14 @@ class AttendDesc(C.Structure):
 
 class FusedDesc(C.Structure):
     _fields_ = [("heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("batch", C.c_int32),
-                ("n_comp", C.c_int32), ("rank_k", C.c_int32), ("rank_v", C.c_int32), ("reserved", C.c_int32),
+                ("n_comp", C.c_int32), ("rank_k", C.c_int32), ("rank_v", C.c_int32), ("tier2_value_rank", C.c_int32),
                 ("tail_cap", C.c_int32), ("n_tail", C.c_int32), ("n_tail_dev", C.c_void_p),
                 ("cluster", C.c_int32), ("context_bf16", C.c_int32),
                 ("left_k", C.c_void_p), ("right_k", C.c_void_p), ("left_v", C.c_void_p), ("right_v", C.c_void_p),
                 ("tail_k", C.c_void_p), ("tail_v", C.c_void_p), ("queries", C.c_void_p),
                 ("importance", C.c_void_p), ("imp_stride", C.c_int64), ("alpha", C.c_double),
                 ("head_avg", C.c_void_p), ("context", C.c_void_p), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_size_t)]
+                ("workspace_bytes", C.c_size_t), ("value_tier", C.c_void_p)]
 
 
 class Profile(C.Structure):

@@ -72,7 +72,7 @@ constexpr int kStreamMinBlocks = KVP_STREAM_MINB;
 #endif
 
 struct Smem {
-  uint32_t ring, phi, plo, pt, stail, part, stats, imps, bars, tslot, total;
+  uint32_t ring, phi, plo, pt, pt2, stail, part, stats, imps, bars, tslot, total;
   uint32_t uloc;  // late-phase alias over [phi, ...), valid once the U MMAs completed
   int uloc_stride;
 };
@@ -86,7 +86,8 @@ __host__ __device__ inline Smem smem_layout(const FusedPlan& p) {
   s.phi = s.ring + p.stages * kRing;
   s.plo = s.phi + p.kpk * np * 128;
   s.pt = align_up(s.plo + p.kpk * np * 128, 1024);  // 2 buffers x {hi, lo} x 2 panels
-  const uint32_t pt_end = s.pt + 8 * np * 128;
+  s.pt2 = s.pt + 8 * np * 128;  // two-tier values: the second tier's p tiles
+  const uint32_t pt_end = s.pt2 + (p.nb2 > 0 ? 8 * np * 128 : 0);
   s.uloc_stride = static_cast<int>(align_up(p.s.rank_v, 4));
   s.uloc = s.phi;
   const uint32_t uloc_end = s.uloc + np * s.uloc_stride * 4;
@@ -558,6 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t ring = smem_addr(smem + L.ring);
       const uint32_t phi = smem_addr(smem + L.phi);
       const uint32_t pt = smem_addr(smem + L.pt);
+      const uint32_t pt2 = smem_addr(smem + L.pt2);
       mbar_wait(&bars[kPopReady], 0);
       tc_fence_after();
       if (a.trace) a.trace[blockIdx.x * 16ull + 8] = global_ns();
@@ -583,6 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&bars[kPFull0 + buf], (t >> 1) & 1);
         tc_fence_after();
         const uint32_t pth = pt + buf * 4 * NP * 128;
+        const uint32_t pth2 = pt2 + buf * 4 * NP * 128;
         for (int mt = 0; mt < p.mtiles; ++mt) {
           const int i0 = it.lv0 + t * p.mtiles + mt, s0 = i0 % NS;
           mbar_wait(&bars[kFull + s0], (i0 / NS) & 1);
@@ -591,6 +594,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int ks = 0; ks < 8; ++ks)
             mma_hilo<ST>(d, smem_desc(ring + s0 * kRing + ks * 2048, kStageBytes, 1024, kSwizzle128B), pth, NP, 2,
                          ks >> 2, (ks & 3) * 32, idesc_u, (t | ks) != 0);
+          if (mt < p.nb2) {  // second value tier: same A tile, its own p image and accumulator
+            const uint32_t d2 = tmem + s_cols + static_cast<uint32_t>((p.mtiles + mt) * NPW);
+            for (int ks = 0; ks < 8; ++ks)
+              mma_hilo<ST>(d2, smem_desc(ring + s0 * kRing + ks * 2048, kStageBytes, 1024, kSwizzle128B), pth2, NP,
+                           2, ks >> 2, (ks & 3) * 32, idesc_u, (t | ks) != 0);
+          }
           mma_commit(&bars[kEmpty + s0]);
         }
         mma_commit(&bars[kPEmpty0 + buf]);
@@ -673,8 +682,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int buf = t & 1;
       if (t >= 2) mbar_wait(&bars[kPEmpty0 + buf], ((t - 2) >> 1) & 1);
       unsigned char* pth = smem + L.pt + buf * 4 * NP * 128;
+      unsigned char* pth2 = smem + L.pt2 + buf * 4 * NP * 128;
       const int row = qd * 32 + lane;  // token within the tile
       const bool valid = t * 128 + row < it.chunk_len;
+      // two-tier values: a second-tier token's p goes to the second image only (U rows < rv2)
+      const bool tier2 = p.nb2 > 0 && valid &&
+                         a.vtier[static_cast<long>(a.inst0 + b) * p.s.n_comp + it.c_first + t * 128 + row] != 0;
 #pragma unroll
       for (int c0 = 0; c0 < gcols; c0 += 4) {
         float v[4];
@@ -684,10 +697,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int h = gbase + c0 + e;
           const float pv = (valid && h < H) ? __expf(v[e] - m_loc[h]) : 0.f;
           zp[c0 + e] += pv;
-          __nv_bfloat16 hi, lo;
+          __nv_bfloat16 hi, lo, zero = __float2bfloat16_rn(0.f);
           split_bf16(pv, hi, lo);
-          *reinterpret_cast<__nv_bfloat16*>(pth + bimg_off(ST, NP, 2, row >> 6, h, row & 63, false)) = hi;
-          *reinterpret_cast<__nv_bfloat16*>(pth + bimg_off(ST, NP, 2, row >> 6, h, row & 63, true)) = lo;
+          *reinterpret_cast<__nv_bfloat16*>(pth + bimg_off(ST, NP, 2, row >> 6, h, row & 63, false)) = tier2 ? zero : hi;
+          *reinterpret_cast<__nv_bfloat16*>(pth + bimg_off(ST, NP, 2, row >> 6, h, row & 63, true)) = tier2 ? zero : lo;
+          if (p.nb2 > 0) {
+            *reinterpret_cast<__nv_bfloat16*>(pth2 + bimg_off(ST, NP, 2, row >> 6, h, row & 63, false)) = tier2 ? hi : zero;
+            *reinterpret_cast<__nv_bfloat16*>(pth2 + bimg_off(ST, NP, 2, row >> 6, h, row & 63, true)) = tier2 ? lo : zero;
+          }
         }
       }
       fence_proxy_async();
@@ -806,6 +823,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int c0 = 0; c0 < gcols; c0 += 4) {
         float v[4] = {0.f, 0.f, 0.f, 0.f};
         if (it.tiles > 0) tld4_hilo<ST>(tmem_row(s_cols + static_cast<uint32_t>(mt * NPW + gbase + c0)), NP, v);
+        if (it.tiles > 0 && mt < p.nb2) {  // second tier contributes to the value-rank prefix only
+          float v2[4];
+          tld4_hilo<ST>(tmem_row(s_cols + static_cast<uint32_t>((p.mtiles + mt) * NPW + gbase + c0)), NP, v2);
+          if (r < p.s.rv2)
+            for (int e = 0; e < 4; ++e) v[e] += v2[e];
+        }
         for (int e = 0; e < 4; ++e) {
           const int h = gbase + c0 + e;
           if (h < H && r < p.s.rank_v) uloc[h * L.uloc_stride + r] = v[e];
@@ -883,11 +906,13 @@ FusedPlan plan_fused(const FusedShape& s) {
   p.heads_per_cta = (s.H + s.cluster - 1) / s.cluster;
   // hi/lo stacked along N (one MMA per A panel) when the doubled tiles fit TMEM;
   // otherwise two MMAs per K step into one tile (e.g. rank 1024)
+  if (s.rv2 < 0 || s.rv2 >= s.rank_v) return bad("tier-2 value rank must be in [0, rank_v)");
+  p.nb2 = s.rv2 > 0 ? (s.rv2 + 127) / 128 : 0;
   p.stack = p.np <= 32;
-  int cols = p.max_tiles * (p.stack ? 2 * p.np : p.np) + p.mtiles * (p.stack ? 2 * p.np : p.np);
+  int cols = (p.max_tiles + p.mtiles + p.nb2) * (p.stack ? 2 * p.np : p.np);
   if (cols > 512 && p.stack) {
     p.stack = false;
-    cols = p.max_tiles * p.np + p.mtiles * p.np;
+    cols = (p.max_tiles + p.mtiles + p.nb2) * p.np;
   }
   if (cols > 512) return bad("TMEM budget exceeded (raise the cluster size)");
   p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
@@ -1138,8 +1163,8 @@ namespace {
 // waves = ceil(batch / co-resident clusters of that size).  Measured on B200
 // for the C2 shape: 6 (1 wave x 3 tiles) beats 4, 5, 7 and 8.
 int auto_cluster(kvp::FusedShape s) {
-  static std::map<std::tuple<int, int, int, int, int, int, int, int>, int> cache;
-  const auto key = std::make_tuple(s.H, s.Hkv, s.D, s.n_comp, s.rank_k, s.rank_v, s.tail_cap, s.batch);
+  static std::map<std::tuple<int, int, int, int, int, int, int, int, int>, int> cache;
+  const auto key = std::make_tuple(s.H, s.Hkv, s.D, s.n_comp, s.rank_k, s.rank_v, s.tail_cap, s.batch, s.rv2);
   if (auto it = cache.find(key); it != cache.end()) return it->second;
   int best = 0;
   long best_cost = 1L << 40;
@@ -1169,6 +1194,7 @@ namespace {
 kvp::FusedShape shape_of(const kvp_fused_desc* d) {
   kvp::FusedShape s{d->heads, d->kv_heads, d->head_dim, d->n_comp, d->rank_k, d->rank_v, 0,
                     d->tail_cap, d->batch, d->cluster};
+  s.rv2 = d->tier2_value_rank;
   if (s.cluster <= 0) s.cluster = auto_cluster(s);
   return s;
 }
@@ -1214,6 +1240,9 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     a.right_v = static_cast<const __nv_bfloat16*>(d->right_v);
     a.tail_k = static_cast<const __nv_bfloat16*>(d->tail_k);
     a.tail_v = static_cast<const __nv_bfloat16*>(d->tail_v);
+    require(d->tier2_value_rank <= 0 || d->value_tier != nullptr, KVP_ERR_PARAMETER,
+            "decode_fused: tier2_value_rank needs the per-token value_tier flags");
+    a.vtier = d->tier2_value_rank > 0 ? d->value_tier : nullptr;
     a.n_tail_dev = d->n_tail_dev;
     a.n_tail = d->n_tail;
     a.q = d->queries;

@@ -19,6 +19,7 @@ struct FusedShape {
   int tail_cap;       // tail rows allocated per instance
   int batch;
   int cluster;        // CTAs per instance in the low-rank core kernel
+  int rv2 = 0;        // two-tier values: rank prefix of the second tier (0 = untiered)
 };
 
 struct FusedArgs {
@@ -31,6 +32,7 @@ struct FusedArgs {
   const __nv_bfloat16* right_v;  // [batch][rank_v][W]
   const __nv_bfloat16* tail_k;   // [batch][tail_cap][W]
   const __nv_bfloat16* tail_v;
+  const unsigned char* vtier;    // [batch][n_comp] nonzero: second value tier (rank prefix rv2); nullable
   const int* n_tail_dev;         // device counter of valid tail rows (nullable)
   int n_tail;                    // used when n_tail_dev == nullptr
   const float* q;                // [batch][q_stride] raw (unscaled) queries (first H*D of each row)
@@ -59,6 +61,7 @@ struct FusedPlan {
   int vpanels;         // V panels, even
   int mtiles;          // vpanels / 2
   int kst;             // ring stages per tile for left_k (panel pairs)
+  int nb2;             // two-tier values: U row tiles that need the second-tier accumulator
   bool stack;          // P / p hi+lo halves stacked along N (np <= 32 and TMEM allows)
   int ntiles;          // 128-token tiles per instance
   int vpanels_st;      // stored V panels (ceil(rank_v / 64))

@@ -45,7 +45,7 @@ def make_case(rng, B, H, Hkv, D, n, rk, rv, nt, cap):
     return case
 
 
-def oracle(case, H, Hkv, D, nt, alpha):
+def oracle(case, H, Hkv, D, nt, alpha, tier=None, rv2=0):
     B, n, _ = case["left_k"].shape
     per = H // Hkv
     ctx = np.zeros((B, H * D))
@@ -53,7 +53,11 @@ def oracle(case, H, Hkv, D, nt, alpha):
     imp = case["imp"].copy()
     for b in range(B):
         K = np.concatenate([case["left_k"][b] @ case["right_k"][b], case["tail_k"][b, :nt]])
-        V = np.concatenate([case["left_v"][b] @ case["right_v"][b], case["tail_v"][b, :nt]])
+        Vc = case["left_v"][b] @ case["right_v"][b]
+        if tier is not None:  # second-tier tokens: value-rank prefix rv2 (store_decompress_row, cache.cpp:63-101)
+            t2 = tier[b] != 0
+            Vc[t2] = case["left_v"][b][t2, :rv2] @ case["right_v"][b][:rv2]
+        V = np.concatenate([Vc, case["tail_v"][b, :nt]])
         for h in range(H):
             g = h // per
             s = K[:, g * D:(g + 1) * D] @ case["q"][b, h * D:(h + 1) * D] / np.sqrt(D)
@@ -66,7 +70,7 @@ def oracle(case, H, Hkv, D, nt, alpha):
     return ctx, ha, imp
 
 
-def run_fused(case, H, Hkv, D, nt, alpha, cluster=0, ld_pad=8):
+def run_fused(case, H, Hkv, D, nt, alpha, cluster=0, ld_pad=8, tier=None, rv2=0):
     torch = _torch()
     from paper_2603_23914_b200 import _capi as capi
     B, n, rk = case["left_k"].shape
@@ -87,6 +91,10 @@ def run_fused(case, H, Hkv, D, nt, alpha, cluster=0, ld_pad=8):
     d = FusedDesc(H, Hkv, D, B, n, rk, rv, 0, cap, nt, None, cluster, 0, t["lk"].data_ptr(), t["rk"].data_ptr(),
                   t["lv"].data_ptr(), t["rv"].data_ptr(), t["tk"].data_ptr(), t["tv"].data_ptr(), t["q"].data_ptr(),
                   t["imp"].data_ptr(), n + cap, alpha, ha.data_ptr(), ctx.data_ptr())
+    if tier is not None:
+        t["tier"] = torch.as_tensor(np.ascontiguousarray(tier, dtype=np.uint8)).cuda()
+        d.tier2_value_rank = rv2
+        d.value_tier = t["tier"].data_ptr()
     capi.lib().kvp_decode_fused.argtypes = [C.POINTER(FusedDesc), C.c_void_p]
     capi.check(capi.lib().kvp_decode_fused(C.byref(d), None))
     torch.cuda.synchronize()
@@ -138,3 +146,37 @@ def test_fused_rejects_rank_beyond_resident_p_image():
     from paper_2603_23914_b200._capi import KvpParameterError
     with pytest.raises(KvpParameterError, match="budget"):
         run_fused(case, H, Hkv, D, nt, 0.25, cluster=cl)
+
+
+TIERED = [
+    # B, H, Hkv, D, n_comp, rank, n_tail, cap, cluster, r1, value fraction of tier 2
+    (1, 32, 32, 128, 2048, 128, 200, 320, 0, 0.25, 0.25),   # C5: VideoLLaVA 8 frames, paper tiering
+    (2, 32, 32, 128, 2048, 128, 70, 320, 8, 0.125, 0.25),
+    (2, 32, 32, 128, 2304, 368, 66, 320, 0, 0.5, 0.25),     # tier boundary inside the first of three U row tiles
+    (1, 32, 32, 128, 4096, 284, 80, 320, 0, 0.375, 0.5),    # second-tier rank 142 spans two U row tiles
+]
+
+
+@pytest.mark.parametrize("shape", TIERED)
+def test_fused_two_tier_values_match_oracle(shape):
+    # Attention-aware decompression (decoder.cpp:105-188): tokens outside the
+    # first group (assign_groups by importance, importance.cpp:67-117) use the
+    # value-rank prefix resolved_tier_rank(fraction, rank) (decoder.cpp:18-23);
+    # key fractions are 1.
+    from oracle import kvpack_oracle as ko
+    B, H, Hkv, D, n, r, nt, cap, cl, r1, vf = shape
+    rng = np.random.default_rng(hash(shape) % 2**32)
+    case = make_case(rng, B, H, Hkv, D, n, r, r, nt, cap)
+    rv2 = ko.resolved_tier_rank(vf, r)
+    tier = np.stack([ko.assign_groups(case["imp"][b, :n], [r1, 1.0 - r1], [r, rv2]) for b in range(B)])
+    ctx, ha, imp = run_fused(case, H, Hkv, D, nt, 0.25, cluster=cl, tier=tier, rv2=rv2)
+    rctx, rha, rimp = oracle(case, H, Hkv, D, nt, 0.25, tier=tier, rv2=rv2)
+    err = np.abs(ctx - rctx).max() / np.abs(rctx).max()
+    print(f"tiered {shape}: rv2 {rv2}, tier-2 tokens {int((tier != 0).sum())}, context max rel err {err:.3e}")
+    assert err <= 1e-3
+    cols = np.r_[np.arange(n), n + np.arange(nt)]
+    assert np.abs(ha[:, cols] - rha).max() <= 1e-4
+    assert np.abs(imp - rimp).max() <= 1e-4
+    # the tiered output differs from the untiered one (the test exercises the second tier)
+    uctx, _, _ = oracle(case, H, Hkv, D, nt, 0.25)
+    assert np.abs(uctx - rctx).max() / np.abs(rctx).max() > 1e-2

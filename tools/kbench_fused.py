@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--ld", type=int, default=0)
+    ap.add_argument("--tier", type=float, default=0.0,
+                    help="two-tier values: first-group ratio r1 (the rest use a quarter of the value rank)")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     B, H, Hkv, D, n, rk, rv, nt, cap = (c[k] for k in ("B", "H", "Hkv", "D", "n", "rk", "rv", "nt", "cap"))
@@ -55,6 +57,11 @@ def main():
                               L["rk"].data_ptr(), L["lv"].data_ptr(), L["rv"].data_ptr(), L["tk"].data_ptr(),
                               L["tv"].data_ptr(), L["q"].data_ptr(), L["imp"].data_ptr(), n + cap, 0.25, None,
                               L["ctx"].data_ptr())
+        if args.tier > 0:
+            rv2 = max(1, min(rv - 1, int(0.25 * rv + 0.5)))
+            L["tier"] = (torch.rand(B, n, device=dev) >= args.tier).to(torch.uint8)
+            L["desc"].tier2_value_rank = rv2
+            L["desc"].value_tier = L["tier"].data_ptr()
         layers.append(L)
     fn = capi.lib().kvp_decode_fused
     fn.argtypes = [C.POINTER(FusedDesc), C.c_void_p]
@@ -109,7 +116,7 @@ def main():
     gbs = B * per_inst / (ms * 1e-3) / 1e9
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("hbm_gbs", 6650.0)
-    print(json.dumps(dict(config=args.config, ms_per_layer=round(ms, 4), bytes_per_layer=B * per_inst,
+    print(json.dumps(dict(config=args.config, tier_r1=args.tier, ms_per_layer=round(ms, 4), bytes_per_layer=B * per_inst,
                           achieved_gbs=round(gbs, 1), peak_gbs=peak, frac=round(gbs / peak, 3))))
 
 
