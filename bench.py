@@ -41,8 +41,10 @@ CONFIGS = {
                geom=(32, 32, 128), layers=32, batch=16, visual=2304, textual=64, steps=256, rank=368),
     "c3": dict(desc="LLaVA-1.5-13B 40 layers, 16 images x 256 tokens + 64 text, batch 64/GPU, 8x compression",
                geom=(40, 40, 128), layers=40, batch=64, visual=4096, textual=64, steps=256, rank=284),
-    "c5": dict(desc="VideoLLaVA-7B 8 frames x 256 tokens + 64 text, batch 32/GPU, rank 128",
-               geom=(32, 32, 128), layers=32, batch=32, visual=2048, textual=64, steps=256, rank=128),
+    "c5": dict(desc="VideoLLaVA-7B 8 frames x 256 tokens + 64 text, batch 32/GPU, rank 128, attention-aware "
+                    "decompression: top 25% of tokens by importance at full rank, the rest at 1/4 of the value rank",
+               geom=(32, 32, 128), layers=32, batch=32, visual=2048, textual=64, steps=256, rank=128,
+               tier=(0.25, 0.25)),
     "c4_8x": dict(desc="Qwen-VL-7B-shaped 16 images x 256 tokens + 64 text, batch 16/GPU, 8x compression",
                   geom=(32, 32, 128), layers=32, batch=16, visual=4096, textual=64, steps=256, rank=256),
 }
@@ -172,7 +174,10 @@ def cpu_reference(cfg, steps, warmup, threads=None):
     """Reference CPU decode step on a bounded sample (oracle/_ref)."""
     from oracle import cpu_baseline as cb
     threads = threads or cb.host_threads()
-    sample = cb.ReferenceSample(cfg["geom"], cfg["visual"], cfg["textual"], cfg["rank"], cfg["rank"], threads)
+    tier = cfg.get("tier")
+    tiering = (((tier[0], 1.0 - tier[0]), (1.0, 1.0), (1.0, tier[1])) if tier else None)
+    sample = cb.ReferenceSample(cfg["geom"], cfg["visual"], cfg["textual"], cfg["rank"], cfg["rank"], threads,
+                                tiering=tiering)
     for _ in range(warmup):
         sample.step()
     secs = [sample.step() for _ in range(steps)]
@@ -232,8 +237,17 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--factor-init", default="compaction", choices=["placeholder", "compaction"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tier", type=float, nargs=2, default=None, metavar=("R1", "VALUE_FRACTION"),
+                    help="two-tier values: first-group ratio and the second group's value-rank fraction "
+                         "(default: the config's; 0 1 = untiered)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.tier is not None:
+        cfg["tier"] = tuple(args.tier)
+    tier = cfg.get("tier")
+    if tier is not None and not (0.0 < tier[0] < 1.0 and tier[1] < 1.0):
+        tier = None
+    cfg["tier"] = tier
     world, rank, local = dist_setup()
     H, Hkv, D = cfg["geom"]
     config_block = {"workload": args.config, "description": cfg["desc"], "heads": H, "kv_heads": Hkv, "head_dim": D,
@@ -241,6 +255,9 @@ def main():
                     "visual_tokens": cfg["visual"], "textual_tokens": cfg["textual"], "rank": cfg["rank"],
                     "tail_tokens_at_timing": None, "l2_flush": "not needed: per-step data >> 126 MB L2",
                     "parallelism": f"instance-sharded x{world} (no data-path collective)"}
+    if tier is not None:
+        config_block["tiering"] = {"ratios": [tier[0], 1.0 - tier[0]], "key_rank_fractions": [1.0, 1.0],
+                                   "value_rank_fractions": [1.0, tier[1]]}
 
     if args.impl == "reference":
         if rank != 0:
@@ -267,7 +284,8 @@ def main():
                       visual_tokens=cfg["visual"], textual_tokens=cfg["textual"],
                       decode_steps=max(cfg["steps"], total_steps), rank_k=cfg["rank"], rank_v=cfg["rank"],
                       visual=ProfileSpec(2 * cfg["rank"], cfg["rank"], 0.98, 1e-2), seed=rank,
-                      factor_init=args.factor_init)
+                      factor_init=args.factor_init,
+                      tier_ratio=tier[0] if tier else 0.0, tier_value_fraction=tier[1] if tier else 1.0)
     if args.factor_init == "compaction":
         warm_libraries(cfg)
     eng = Engine(spec)

@@ -232,7 +232,7 @@ typedef struct {
 /* WorkloadSpec + DecodeConfig subset of the serving layout (harness.hpp:27-38,
  * decoder.hpp:53-75): visual segment factored at rank_k / rank_v right after
  * prefill (compress_now), textual segment dense, decode tokens join the
- * textual tail, importance EMA with `alpha`, untiered decompression. */
+ * textual tail, importance EMA with `alpha`, untiered or two-tier value decompression. */
 typedef struct {
   int32_t heads, kv_heads, head_dim;
   int32_t layers, batch;
@@ -246,6 +246,11 @@ typedef struct {
   int32_t svd_oversampling, svd_power_iterations;
   int32_t factor_init;          /* 0: compaction of the generated K/V; 1: placeholder factors */
   int32_t cluster;              /* CTAs per instance in the decode core, 0 = auto */
+  /* two-tier attention-aware decompression of the visual block (TierSpec, decoder.hpp:31-52): each step the
+     first tier_ratio of the tokens by importance (assign_groups) keep the full value rank, the rest use
+     resolved_tier_rank(tier_value_fraction, rank_v); key fractions 1.  tier_ratio 0 or fraction 1 = untiered */
+  double tier_ratio;
+  double tier_value_fraction;
 } kvp_engine_config;
 
 typedef struct {

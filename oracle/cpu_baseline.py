@@ -32,12 +32,12 @@ def _low_rank_kv(rng, tokens, width, rank):
 
 
 class ReferenceSample:
-    def __init__(self, geom, visual_tokens, textual_tokens, rank_k, rank_v, threads, seed=0):
+    def __init__(self, geom, visual_tokens, textual_tokens, rank_k, rank_v, threads, seed=0, tiering=None):
         H, Hkv, D = geom
         self.geom = geom
         self.threads = threads
         W, HD = Hkv * D, H * D
-        self.ini = decode_ini(ranks=(rank_k, rank_v, 0, 0), period=512, svd="randomized")
+        self.ini = decode_ini(ranks=(rank_k, rank_v, 0, 0), tiering=tiering, period=512, svd="randomized")
         rng = np.random.default_rng(seed)
         s = 1.0 / np.sqrt(HD)
         self.weights = [rng.standard_normal(sh).astype(np.float32) * s for sh in ((HD, HD), (HD, W), (HD, W), (HD, HD))]

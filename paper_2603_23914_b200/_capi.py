@@ -89,7 +89,8 @@ class EngineConfig(C.Structure):
                 ("decode_steps", C.c_int32), ("rank_k", C.c_int32), ("rank_v", C.c_int32), ("alpha", C.c_double),
                 ("seed", C.c_uint64), ("visual", Profile), ("textual", Profile), ("svd_method", C.c_int32),
                 ("svd_seed", C.c_uint64), ("svd_oversampling", C.c_int32), ("svd_power_iterations", C.c_int32),
-                ("factor_init", C.c_int32), ("cluster", C.c_int32)]
+                ("factor_init", C.c_int32), ("cluster", C.c_int32), ("tier_ratio", C.c_double),
+                ("tier_value_fraction", C.c_double)]
 
 
 class EngineInfo(C.Structure):

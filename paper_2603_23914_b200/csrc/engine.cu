@@ -42,6 +42,10 @@ struct kvp_engine {
   float *qkv = nullptr, *q = nullptr, *xin = nullptr, *xcur = nullptr, *yout = nullptr;
   int* n_tail_dev = nullptr;
   void* fused_ws = nullptr;
+  // two-tier values (TierSpec): second-group value rank, first-group ratio, per-token flags
+  int rv2 = 0;
+  double tier_ratio = 0.0;
+  unsigned char* vtier = nullptr;
   size_t fused_ws_bytes = 0;
   kvp::FusedPlan plan{};   // whole batch (workspace, tensor maps)
   kvp::FusedPlan gplan{};  // one instance group (launch grids)
@@ -206,6 +210,7 @@ FusedArgs fused_args(kvp_engine* e, int l) {
   a.head_avg = nullptr;
   a.ctx_out = e->ctx;
   a.ctx_bf16 = 1;
+  a.vtier = e->vtier ? e->vtier + static_cast<size_t>(lidx) * e->B * e->n : nullptr;
   a.ws_pimg = static_cast<unsigned char*>(e->fused_ws);
   a.ws_tail = reinterpret_cast<float*>(a.ws_pimg + static_cast<size_t>(e->B) * 2 * e->plan.kpk * e->plan.np * 128);
   a.ws_u = a.ws_tail + static_cast<size_t>(e->B) * e->H * e->cap;
@@ -244,6 +249,20 @@ void enqueue_attention(kvp_engine* e, int l) {
   KVP_CUDA(cudaStreamWaitEvent(s, e->ev_join, 0));
 }
 
+// resolve_tiering (decoder.cpp:105-139) for the next step of every layer: assign_groups
+// over each table's compressed tokens (importance.cpp:67-117) -> per-token second-tier
+// flags.  A step's plan uses the importance as the previous step's EMA left it, so one
+// launch over all L x B tables at the end of a step (and after prefill / reset) serves
+// the whole next step.
+void assign_all_tiers(kvp_engine* e, cudaStream_t s) {
+  if (e->rv2 <= 0) return;
+  const double ratios[2] = {e->tier_ratio, 1.0 - e->tier_ratio};
+  const int32_t kr[2] = {e->rk, e->rk}, vr[2] = {e->rv, e->rv2};
+  const int rc = kvp_assign_tiers(e->L * e->B, e->n, e->imp, static_cast<int64_t>(e->imp_stride()), 2, ratios, kr,
+                                  vr, e->vtier, nullptr, nullptr, s);
+  if (rc != KVP_OK) fail(rc, kvp_last_error_message());
+}
+
 // One decode step over all layers, enqueued on e->stream (graph-capturable).
 void enqueue_step(kvp_engine* e) {
   cudaStream_t s = e->stream;
@@ -259,6 +278,7 @@ void enqueue_step(kvp_engine* e) {
     gemm_bf16(e, e->B, e->HD, e->HD, e->ctx, e->wo + static_cast<size_t>(l) * e->HD * e->HD, e->HD,
               last ? static_cast<void*>(e->yout) : static_cast<void*>(e->xb), !last);
   }
+  assign_all_tiers(e, s);
 }
 
 __global__ void gauss_f32_kernel(float* out, long n, uint64_t seed, uint64_t stream, uint64_t offset) {
@@ -447,6 +467,18 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     e->rv = std::min(c->rank_v, std::min(e->n, e->W));
     e->ld = 0;
     FusedShape fs{e->H, e->Hkv, e->D, e->n, e->rk, e->rv, e->ld, e->cap, e->B, c->cluster};
+    require(c->tier_ratio >= 0.0 && c->tier_ratio <= 1.0 && c->tier_value_fraction >= 0.0 &&
+                c->tier_value_fraction <= 1.0,
+            KVP_ERR_PARAMETER, "engine: tier ratio and value fraction must be in [0, 1]");
+    if (c->tier_ratio > 0.0 && c->tier_ratio < 1.0) {
+      // resolved_tier_rank (decoder.cpp:18-23): clamp(floor(f * R + 0.5), 1, R)
+      const int r2 = std::min(std::max(static_cast<int>(std::floor(c->tier_value_fraction * e->rv + 0.5)), 1), e->rv);
+      if (r2 < e->rv) {
+        e->rv2 = r2;
+        e->tier_ratio = c->tier_ratio;
+      }
+    }
+    fs.rv2 = e->rv2;
     if (fs.cluster <= 0) fs.cluster = auto_cluster_size(fs);
     e->plan = plan_fused(fs);
     require(e->plan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->plan.why).c_str());
@@ -489,6 +521,7 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     e->n_tail_dev = e->alloc<int>(1);
     e->fused_ws_bytes = fused_workspace_bytes(fs);
     e->fused_ws = e->alloc<char>(e->fused_ws_bytes);
+    if (e->rv2 > 0) e->vtier = e->alloc<unsigned char>(static_cast<size_t>(e->L) * e->B * e->n);
     KVP_CUDA(cudaMemset(e->fused_ws, 0, e->fused_ws_bytes));
     *out = e.release();
   });
@@ -565,6 +598,7 @@ extern "C" int kvp_engine_prefill(kvp_engine* e) {
     }
     KVP_CUDA(cudaEventRecord(e1, s));
     KVP_CUDA(cudaMemsetAsync(e->imp, 0, sizeof(double) * e->L * e->B * e->imp_stride(), s));
+    assign_all_tiers(e, s);
     KVP_CUDA(cudaMemcpyAsync(e->n_tail_dev, &e->t0, sizeof(int), cudaMemcpyHostToDevice, s));
     KVP_CUDA(cudaStreamSynchronize(s));
     float ms = 0.f;
@@ -619,6 +653,7 @@ extern "C" int kvp_engine_reset_steps(kvp_engine* e) {
   return guarded([&] {
     require(e != nullptr, KVP_ERR_PARAMETER, "engine: null");
     KVP_CUDA(cudaMemcpyAsync(e->n_tail_dev, &e->t0, sizeof(int), cudaMemcpyHostToDevice, e->stream));
+    assign_all_tiers(e, e->stream);
     KVP_CUDA(cudaStreamSynchronize(e->stream));
     e->steps_taken = 0;
   });
@@ -700,10 +735,12 @@ extern "C" int kvp_engine_time_attention(kvp_engine* e, int32_t iters, double* m
     int nt = 0;
     KVP_CUDA(cudaMemcpy(&nt, e->n_tail_dev, sizeof(int), cudaMemcpyDeviceToHost));
     *ms_per_layer = ms / (static_cast<double>(iters) * e->L);
-    // s*[n*(Rk+Rv) + (Rk+Rv)*W + 2*T_uc*W] + 16*T per instance (append excluded)
-    const double per = 2.0 * (static_cast<double>(e->n) * (e->rk + e->rv) + static_cast<double>(e->rk + e->rv) * e->W +
-                              2.0 * nt * e->W) +
-                       16.0 * (e->n + nt);
+    // s*[sum_f n_f*(Rk_f+Rv_f) + (Rk+Rv)*W + 2*T_uc*W] + 16*T per instance (append excluded);
+    // two tiers: n_1 = floor(r_1 n + 0.5) tokens at full rank, the rest at value rank rv2 (group_sizes,
+    // importance.cpp:98-110)
+    const double n1 = e->rv2 > 0 ? std::floor(e->tier_ratio * e->n + 0.5) : static_cast<double>(e->n);
+    const double coef = n1 * (e->rk + e->rv) + (e->n - n1) * (e->rk + (e->rv2 > 0 ? e->rv2 : e->rv));
+    const double per = 2.0 * (coef + static_cast<double>(e->rk + e->rv) * e->W + 2.0 * nt * e->W) + 16.0 * (e->n + nt);
     *bytes_per_layer = per * e->B;
   });
 }

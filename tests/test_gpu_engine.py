@@ -49,13 +49,14 @@ def unpack_left(raw_u8, B, n, rank):
     return vals.transpose(0, 1, 3, 2, 4).reshape(B, tiles * 128, panels * 64)[:, :n, :rank]
 
 
-def make_engine(factor_init="compaction"):
+def make_engine(factor_init="compaction", tier=None):
     from paper_2603_23914_b200.engine import Engine, EngineSpec, ProfileSpec
     s = SPEC
     spec = EngineSpec(heads=s["H"], kv_heads=s["Hkv"], head_dim=s["D"], layers=s["L"], batch=s["B"],
                       visual_tokens=s["n"], textual_tokens=s["t0"], decode_steps=s["steps"], rank_k=s["rank"],
                       rank_v=s["rank"], seed=s["seed"], visual=ProfileSpec(24, 8, 0.9, 1e-2),
-                      textual=ProfileSpec(6, 2, 0.9, 1e-3), factor_init=factor_init, svd_seed=3)
+                      textual=ProfileSpec(6, 2, 0.9, 1e-3), factor_init=factor_init, svd_seed=3,
+                      tier_ratio=tier[0] if tier else 0.0, tier_value_fraction=tier[1] if tier else 1.0)
     eng = Engine(spec)
     eng.prefill()
     return eng
@@ -109,18 +110,22 @@ def test_compaction_reconstructs_visual_segments():
     eng.close()
 
 
-def test_decode_steps_match_reference():
+@pytest.mark.parametrize("tier", [None, (0.5, 0.25)], ids=["untiered", "two_tier"])
+def test_decode_steps_match_reference(tier):
     """Engine decode vs the reference decode_step (double) on the engine's own
-    bf16 factors, layer by layer, 4 steps, both instances."""
+    bf16 factors, layer by layer, 4 steps, both instances; untiered, and with
+    two-tier attention-aware value decompression (the reference's [decode.tiering]:
+    half the tokens by importance at full rank, the rest at a quarter of the value rank)."""
     torch = _torch()
     from oracle import ref
     from oracle.cases import decode_ini
     s = SPEC
     H, Hkv, D, L, B = s["H"], s["Hkv"], s["D"], s["L"], s["B"]
     W, HD = Hkv * D, H * D
-    eng = make_engine()
+    eng = make_engine(tier=tier)
     states = [layer_state(eng, l) for l in range(L)]
-    ini = decode_ini(ranks=(s["rank"], s["rank"], 0, 0), period=None, alpha=0.25)
+    tiering = ((tier[0], 1.0 - tier[0]), (1.0, 1.0), (1.0, tier[1])) if tier else None
+    ini = decode_ini(ranks=(s["rank"], s["rank"], 0, 0), tiering=tiering, period=None, alpha=0.25)
     # reference caches seeded with the engine's factors: visual block via compress_now of
     # the exact reconstruction (rank-16 exact), textual tail verbatim
     caches = {}
