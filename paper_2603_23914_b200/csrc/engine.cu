@@ -11,6 +11,7 @@
 //   ctx (bf16) --GEMM--> x_{l+1}                (decoder.cpp:590)
 // The whole step is captured once into a CUDA graph and replayed; the tail
 // length lives in a device counter so the graph is static.
+#include <cublasLt.h>
 #include <cublas_v2.h>
 #include <cuda_bf16.h>
 
@@ -33,6 +34,15 @@ struct kvp_engine {
   cudaStream_t stream = nullptr;
   cublasHandle_t blas = nullptr;
   void* blas_ws = nullptr;
+  // projection GEMMs through cuBLASLt with the algorithm timed fastest at engine creation
+  struct LtGemm {
+    cublasLtMatmulDesc_t op = nullptr;
+    cublasLtMatrixLayout_t a = nullptr, b = nullptr, c = nullptr;
+    cublasLtMatmulAlgo_t algo{};
+    bool ok = false;
+  };
+  cublasLtHandle_t lt = nullptr;
+  LtGemm g_qkv, g_o, g_o_last;
   // buffers
   __nv_bfloat16 *wqkv = nullptr, *wo = nullptr;
   unsigned char *lk = nullptr, *lv = nullptr;  // packed left factors [L][...]
@@ -73,6 +83,12 @@ struct kvp_engine {
     if (graph) cudaGraphDestroy(graph);
     for (void* p : allocations) cudaFree(p);
     if (blas) cublasDestroy(blas);
+    for (LtGemm* g : {&g_qkv, &g_o, &g_o_last}) {
+      if (g->op) cublasLtMatmulDescDestroy(g->op);
+      for (cublasLtMatrixLayout_t l : {g->a, g->b, g->c})
+        if (l) cublasLtMatrixLayoutDestroy(l);
+    }
+    if (lt) cublasLtDestroy(lt);
     for (cudaEvent_t ev : {ev_fork, ev_q0, ev_join})
       if (ev) cudaEventDestroy(ev);
     if (stream2) cudaStreamDestroy(stream2);
@@ -180,9 +196,69 @@ void launch_1d(long n, auto&& f) {
 
 // Row-major C (m x n) = A (m x k, bf16) * B (k x n, bf16), fp32 accumulate;
 // C is fp32 or bf16 (the next layer's input needs no separate cast).
+constexpr size_t kBlasWs = 32u << 20;
+
+// Row-major C (m x n) = A (m x k) B (k x n), bf16 operands, fp32 accumulate, through
+// cuBLASLt (column-major C^T = B^T A^T).  Among the heuristic's candidates the one
+// timed fastest on this shape is kept (`tune`); cublasGemmEx's default otherwise.
+void lt_setup(kvp_engine* e, kvp_engine::LtGemm& g, int m, int n, int k, bool c_bf16, const __nv_bfloat16* a,
+              const __nv_bfloat16* b, void* c) {
+  if (!e->lt && cublasLtCreate(&e->lt) != CUBLAS_STATUS_SUCCESS) return;
+  if (cublasLtMatmulDescCreate(&g.op, CUBLAS_COMPUTE_32F, CUDA_R_32F) != CUBLAS_STATUS_SUCCESS) return;
+  if (cublasLtMatrixLayoutCreate(&g.b, CUDA_R_16BF, n, k, n) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatrixLayoutCreate(&g.a, CUDA_R_16BF, k, m, k) != CUBLAS_STATUS_SUCCESS ||
+      cublasLtMatrixLayoutCreate(&g.c, c_bf16 ? CUDA_R_16BF : CUDA_R_32F, n, m, n) != CUBLAS_STATUS_SUCCESS)
+    return;
+  cublasLtMatmulPreference_t pref = nullptr;
+  cublasLtMatmulPreferenceCreate(&pref);
+  size_t ws = kBlasWs;
+  cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws, sizeof(ws));
+  cublasLtMatmulHeuristicResult_t res[16];
+  int count = 0;
+  cublasLtMatmulAlgoGetHeuristic(e->lt, g.op, g.b, g.a, g.c, g.c, pref, 16, res, &count);
+  cublasLtMatmulPreferenceDestroy(pref);
+  if (count <= 0) return;
+  const float one = 1.f, zero = 0.f;
+  cudaEvent_t e0, e1;
+  KVP_CUDA(cudaEventCreate(&e0));
+  KVP_CUDA(cudaEventCreate(&e1));
+  float best = 1e30f;
+  for (int i = 0; i < count; ++i) {
+    if (res[i].state != CUBLAS_STATUS_SUCCESS) continue;
+    bool fine = true;
+    for (int rep = 0; rep < 3 && fine; ++rep)  // warm-up
+      fine = cublasLtMatmul(e->lt, g.op, &one, b, g.b, a, g.a, &zero, c, g.c, c, g.c, &res[i].algo, e->blas_ws,
+                            kBlasWs, e->stream) == CUBLAS_STATUS_SUCCESS;
+    if (!fine) continue;
+    KVP_CUDA(cudaEventRecord(e0, e->stream));
+    for (int rep = 0; rep < 20; ++rep)
+      cublasLtMatmul(e->lt, g.op, &one, b, g.b, a, g.a, &zero, c, g.c, c, g.c, &res[i].algo, e->blas_ws, kBlasWs,
+                     e->stream);
+    KVP_CUDA(cudaEventRecord(e1, e->stream));
+    KVP_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    KVP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms < best) {
+      best = ms;
+      g.algo = res[i].algo;
+      g.ok = true;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGetLastError();
+}
+
 void gemm_bf16(kvp_engine* e, int m, int n, int k, const __nv_bfloat16* a, const __nv_bfloat16* b, int ldb, void* c,
                bool c_bf16) {
   const float one = 1.f, zero = 0.f;
+  kvp_engine::LtGemm* g = n == e->HD + 2 * e->W ? &e->g_qkv : (c_bf16 ? &e->g_o : &e->g_o_last);
+  if (g->ok && ldb == n && m == e->B) {
+    blas_check(cublasLtMatmul(e->lt, g->op, &one, b, g->b, a, g->a, &zero, c, g->c, c, g->c, &g->algo, e->blas_ws,
+                              kBlasWs, e->stream),
+               "cublasLtMatmul");
+    return;
+  }
   blas_check(cublasGemmEx(e->blas, CUBLAS_OP_N, CUBLAS_OP_N, n, m, k, &one, b, CUDA_R_16BF, ldb, a, CUDA_R_16BF, k,
                           &zero, c, c_bf16 ? CUDA_R_16BF : CUDA_R_32F, n, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
              "cublasGemmEx");
@@ -498,9 +574,8 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
       KVP_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     blas_check(cublasCreate(&e->blas), "cublasCreate");
     blas_check(cublasSetStream(e->blas, e->stream), "cublasSetStream");
-    const size_t blas_ws = 32u << 20;
-    e->blas_ws = e->alloc<char>(blas_ws);
-    blas_check(cublasSetWorkspace(e->blas, e->blas_ws, blas_ws), "cublasSetWorkspace");
+    e->blas_ws = e->alloc<char>(kBlasWs);
+    blas_check(cublasSetWorkspace(e->blas, e->blas_ws, kBlasWs), "cublasSetWorkspace");
     const size_t L = e->L;
     e->wqkv = e->alloc<__nv_bfloat16>(L * e->HD * (e->HD + 2 * e->W));
     e->wo = e->alloc<__nv_bfloat16>(L * e->HD * e->HD);
@@ -521,6 +596,13 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     e->n_tail_dev = e->alloc<int>(1);
     e->fused_ws_bytes = fused_workspace_bytes(fs);
     e->fused_ws = e->alloc<char>(e->fused_ws_bytes);
+    if (!(std::getenv("KVP_LT") && std::atoi(std::getenv("KVP_LT")) == 0)) {
+      const int nqkv = e->HD + 2 * e->W;
+      lt_setup(e.get(), e->g_qkv, e->B, nqkv, e->HD, false, e->xb, e->wqkv, e->qkv);
+      lt_setup(e.get(), e->g_o, e->B, e->HD, e->HD, true, e->ctx, e->wo, e->xb);
+      lt_setup(e.get(), e->g_o_last, e->B, e->HD, e->HD, false, e->ctx, e->wo, e->yout);
+      KVP_CUDA(cudaStreamSynchronize(e->stream));
+    }
     if (e->rv2 > 0) e->vtier = e->alloc<unsigned char>(static_cast<size_t>(e->L) * e->B * e->n);
     KVP_CUDA(cudaMemset(e->fused_ws, 0, e->fused_ws_bytes));
     *out = e.release();
