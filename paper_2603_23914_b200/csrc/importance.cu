@@ -12,6 +12,8 @@
 #include "common.cuh"
 #include "importance.cuh"
 
+#include <cstdlib>
+
 namespace kvp {
 
 // s_j <- decay*s_j + blend*mean_t attn[t][j]; one thread per (table, j).
@@ -122,6 +124,128 @@ __global__ void tier_kernel(int n, int npow2, const double* __restrict__ scores,
   }
 }
 
+// One CTA per table, n <= kSelThreads * kSelPer: radix select instead of a sort.
+// Rank order is (key ascending = score descending, index ascending).  For each
+// group boundary b_f the b_f-th smallest key D* is found with eight 8-bit digit
+// passes over the keys held in registers; a token is inside the boundary when
+// its key is below D*, or equal to it and among the first (b_f - #below) such
+// tokens by index (block-wide prefix count).  Its group is the number of
+// boundaries it falls outside of.  Same result as the sort, bit for bit.
+constexpr int kSelThreads = 512, kSelPer = 8;
+__device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned* wsum, unsigned* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    unsigned w = lane < nw ? wsum[lane] : 0u, wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += y;
+    }
+    if (lane < nw) wsum[lane] = wi - w;
+    if (lane == nw - 1) *total = wi;
+  }
+  __syncthreads();
+  const unsigned r = wsum[warp] + inc - v;
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(kSelThreads) tier_select_kernel(int n, const double* __restrict__ scores, long stride,
+                                                                  int n_groups, TierParams tp, uint8_t* tier_out,
+                                                                  uint16_t* rk_out, uint16_t* rv_out) {
+  __shared__ unsigned hist[256];
+  __shared__ unsigned sel[2];
+  __shared__ unsigned wsum[32];
+  __shared__ unsigned total;
+  const double* sc = scores + (long)blockIdx.x * stride;
+  const int base = threadIdx.x * kSelPer;  // a contiguous chunk of indices per thread
+  const int lane = threadIdx.x & 31;
+  uint64_t key[kSelPer];
+  int grp[kSelPer];
+#pragma unroll
+  for (int j = 0; j < kSelPer; ++j) {
+    key[j] = base + j < n ? desc_key(sc[base + j]) : 0ull;
+    grp[j] = 0;
+  }
+  for (int f = 1; f < n_groups; ++f) {
+    const int k = tp.bounds[f];
+    if (k >= n) continue;  // everybody inside
+    if (k <= 0) {
+#pragma unroll
+      for (int j = 0; j < kSelPer; ++j) grp[j] += 1;
+      continue;
+    }
+    uint64_t prefix = 0, mask = 0;
+    unsigned remaining = static_cast<unsigned>(k);
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int i = threadIdx.x; i < 256; i += blockDim.x) hist[i] = 0u;
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < kSelPer; ++j)
+        if (base + j < n && (key[j] & mask) == prefix) atomicAdd(&hist[(key[j] >> shift) & 255u], 1u);
+      __syncthreads();
+      if (threadIdx.x < 32) {
+        unsigned own = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) own += hist[lane * 8 + b];
+        unsigned inc = own;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += y;
+        }
+        const unsigned before = inc - own;
+        if (before < remaining && remaining <= inc) {
+          unsigned cum = before;
+          for (int b = 0; b < 8; ++b) {
+            const unsigned h = hist[lane * 8 + b];
+            if (cum + h >= remaining) {
+              sel[0] = static_cast<unsigned>(lane * 8 + b);
+              sel[1] = remaining - cum;
+              break;
+            }
+            cum += h;
+          }
+        }
+      }
+      __syncthreads();
+      prefix |= static_cast<uint64_t>(sel[0]) << shift;
+      mask |= 255ull << shift;
+      remaining = sel[1];
+      __syncthreads();
+    }
+    // ties with the boundary key: the first `remaining` of them by index are inside
+    unsigned eq = 0;
+#pragma unroll
+    for (int j = 0; j < kSelPer; ++j) eq += (base + j < n && key[j] == prefix) ? 1u : 0u;
+    unsigned order = block_exclusive_scan(eq, wsum, &total);
+#pragma unroll
+    for (int j = 0; j < kSelPer; ++j) {
+      bool inside = key[j] < prefix;
+      if (base + j < n && key[j] == prefix) inside = order++ < remaining;
+      if (!inside) grp[j] += 1;
+    }
+  }
+  const long out = (long)blockIdx.x * n;
+#pragma unroll
+  for (int j = 0; j < kSelPer; ++j) {
+    const int t = base + j;
+    if (t >= n) break;
+    if (tier_out) tier_out[out + t] = static_cast<uint8_t>(grp[j]);
+    if (rk_out) rk_out[out + t] = static_cast<uint16_t>(tp.rank_k[grp[j]]);
+    if (rv_out) rv_out[out + t] = static_cast<uint16_t>(tp.rank_v[grp[j]]);
+  }
+}
+
 TierParams make_tier_params(int n, int n_groups, const double* ratios, const int32_t* key_ranks,
                             const int32_t* value_ranks) {
   require(n_groups >= 1 && n_groups <= kMaxTiers, KVP_ERR_PARAMETER,
@@ -160,6 +284,12 @@ TierParams make_tier_params(int n, int n_groups, const double* ratios, const int
 void launch_tiers(int n_tables, int n, const double* scores, long stride, int n_groups, const TierParams& tp,
                   uint8_t* tier_out, uint16_t* rk_out, uint16_t* rv_out, cudaStream_t s) {
   if (n == 0 || n_tables == 0) return;
+  static const bool force_sort = std::getenv("KVP_TIER_SORT") != nullptr;  // A/B: the bitonic sort
+  if (n <= kSelThreads * kSelPer && !force_sort) {
+    tier_select_kernel<<<n_tables, kSelThreads, 0, s>>>(n, scores, stride, n_groups, tp, tier_out, rk_out, rv_out);
+    KVP_LAUNCHED();
+    return;
+  }
   int npow2 = 1;
   while (npow2 < n) npow2 <<= 1;
   const size_t smem = (size_t)npow2 * (sizeof(uint64_t) + sizeof(uint32_t));

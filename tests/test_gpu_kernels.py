@@ -93,3 +93,32 @@ def test_assign_tiers_device_batched(torch_cuda):
         want = ko.assign_groups(s[t], [0.25, 0.75], [368, 92])
         assert np.array_equal(tier[t].cpu().numpy(), want)
         assert np.array_equal(rv[t].cpu().numpy(), np.where(want == 0, 368, 92))
+
+
+@pytest.mark.parametrize("n", [1, 7, 100, 513, 2048, 4096, 5000])
+def test_assign_tiers_select_matches_oracle(torch_cuda, n):
+    """The radix-select path (n <= 4096) and the sort path (larger n) against the
+    reference ordering (importance.cpp:67-117): heavy ties, zeros and -0.0,
+    three and four groups, empty groups."""
+    torch = torch_cuda
+    from oracle import kvpack_oracle as ko
+    from paper_2603_23914_b200 import _capi as capi
+    rng = np.random.default_rng(n)
+    tables = 6
+    s = np.round(rng.uniform(0, 1, (tables, n)), 2)  # many exact ties
+    s[0] = 0.0
+    s[1, ::3] = -0.0
+    s[2, : n // 2] = 1e-300
+    ds = torch.as_tensor(s).cuda()
+    for ratios in ([0.25, 0.75], [0.125, 0.375, 0.5], [0.0, 0.5, 0.0, 0.5], [1.0, 0.0]):
+        g = len(ratios)
+        ranks = np.array(sorted(rng.integers(1, 64, g), reverse=True), dtype=np.int32)
+        tier = torch.zeros((tables, n), dtype=torch.uint8, device="cuda")
+        r = np.ascontiguousarray(ratios, dtype=np.float64)
+        capi.call("kvp_assign_tiers", tables, n, ds.data_ptr(), n, g, r.ctypes.data, ranks.ctypes.data,
+                  ranks.ctypes.data, tier.data_ptr(), None, None, None)
+        torch.cuda.synchronize()
+        got = tier.cpu().numpy()
+        for t in range(tables):
+            want = ko.assign_groups(s[t], list(ratios), list(ranks))
+            assert np.array_equal(got[t], want), (n, ratios, t)
