@@ -10,15 +10,26 @@ import json
 import re
 
 
-def summarise(path):
+def summarise(path, from_kernel=None, launches=None):
+    """Per-kernel shares.  from_kernel / launches: keep only the `launches`
+    launches that start at the first launch whose name contains `from_kernel`
+    (e.g. the decode steps after the engine's cuBLASLt tuning)."""
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
     hdr = rows[hi]
     idx = {h: i for i, h in enumerate(hdr)}
+    body = [r for r in rows[hi + 1:] if len(r) >= len(hdr)]
+    if from_kernel:
+        ids = []
+        for r in body:
+            if r[idx["ID"]] not in ids:
+                ids.append(r[idx["ID"]])
+        names = {r[idx["ID"]]: r[idx["Kernel Name"]] for r in body}
+        start = next(i for i, k in enumerate(ids) if from_kernel in names[k])
+        keep = set(ids[start:start + launches] if launches else ids[start:])
+        body = [r for r in body if r[idx["ID"]] in keep]
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
-    for r in rows[hi + 1:]:
-        if len(r) < len(hdr):
-            continue
+    for r in body:
         name = re.sub(r"\(.*", "", r[idx["Kernel Name"]]).strip()[:80]
         metric, val = r[idx["Metric Name"]], float(r[idx["Metric Value"]].replace(",", ""))
         if metric == "gpu__time_duration.sum":
@@ -39,8 +50,10 @@ if __name__ == "__main__":
     ap.add_argument("csv")
     ap.add_argument("out", nargs="?")
     ap.add_argument("--command", default=None)
+    ap.add_argument("--from-kernel", default=None)
+    ap.add_argument("--launches", type=int, default=None)
     a = ap.parse_args()
-    s = summarise(a.csv)
+    s = summarise(a.csv, a.from_kernel, a.launches)
     s["command"] = a.command
     s["note"] = "ncu per-launch times are cold-cache and serialised: compare shares, not absolutes"
     text = json.dumps(s, indent=1)
