@@ -539,6 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int per_tile = is_v ? p.mtiles : p.kst;
         const int tile = rel / per_tile, pair = rel % per_tile;
         if (a.trace && i == it.lv0) a.trace[blockIdx.x * 16ull + 10] = global_ns();
+        if (a.trace && i == it.total - 1) a.trace[blockIdx.x * 16ull + 14] = global_ns();  // last stage issued
         // packed panel-major layout: the panels (2 pair, 2 pair + 1) of a tile are contiguous;
         // a missing odd V panel stays unloaded (U rows >= rank_v are never read)
         const long gtile = static_cast<long>(a.inst0 + b) * p.ntiles + it.tile0 + tile;
@@ -584,6 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int buf = t & 1;
         mbar_wait(&bars[kPFull0 + buf], (t >> 1) & 1);
         tc_fence_after();
+        if (a.trace && t < 3) a.trace[blockIdx.x * 16ull + 11 + t] = global_ns();  // p tile t seen by the MMA
         const uint32_t pth = pt + buf * 4 * NP * 128;
         const uint32_t pth2 = pt2 + buf * 4 * NP * 128;
         for (int mt = 0; mt < p.mtiles; ++mt) {
@@ -604,6 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(&bars[kPEmpty0 + buf]);
       }
+      if (a.trace) a.trace[blockIdx.x * 16ull + 7] = global_ns();  // last U MMA issued
       mma_commit(&bars[kUFull]);
       mbar_wait(&bars[kTmemFree], 0);
     }
