@@ -47,6 +47,10 @@ CONFIGS = {
                tier=(0.25, 0.25)),
     "c4_8x": dict(desc="Qwen-VL-7B-shaped 16 images x 256 tokens + 64 text, batch 16/GPU, 8x compression",
                   geom=(32, 32, 128), layers=32, batch=16, visual=4096, textual=64, steps=256, rank=256),
+    "c4_4x": dict(desc="Qwen-VL-7B-shaped 16 images x 256 tokens + 64 text, batch 16/GPU, 4x compression",
+                  geom=(32, 32, 128), layers=32, batch=16, visual=4096, textual=64, steps=256, rank=512),
+    "c4_2x": dict(desc="Qwen-VL-7B-shaped 16 images x 256 tokens + 64 text, batch 16/GPU, 2x compression",
+                  geom=(32, 32, 128), layers=32, batch=16, visual=4096, textual=64, steps=256, rank=1024),
 }
 METRIC = "decode tokens/sec over compressed KV-cache"
 

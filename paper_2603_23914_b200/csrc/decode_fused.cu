@@ -85,9 +85,13 @@ __host__ __device__ inline Smem smem_layout(const FusedPlan& p) {
   s.ring = 0;
   s.phi = s.ring + p.stages * kRing;
   s.plo = s.phi + p.kpk * np * 128;
-  s.pt = align_up(s.plo + p.kpk * np * 128, 1024);  // 2 buffers x {hi, lo} x 2 panels
+  // p tiles: 2 buffers x {hi, lo} x 2 panels (x 2 for the second value tier).  For large
+  // ranks (pt_alias) they reuse the P image's bytes: the image is dead once the S MMAs
+  // completed, which precedes the first p tile.
+  const uint32_t pimg_bytes = 2 * p.kpk * np * 128, pt_bytes = 8 * np * 128 * (p.nb2 > 0 ? 2 : 1);
+  s.pt = p.pt_alias ? s.phi : align_up(s.phi + pimg_bytes, 1024);
   s.pt2 = s.pt + 8 * np * 128;  // two-tier values: the second tier's p tiles
-  const uint32_t pt_end = s.pt2 + (p.nb2 > 0 ? 8 * np * 128 : 0);
+  const uint32_t pt_end = (s.pt + pt_bytes) > (s.phi + pimg_bytes) ? s.pt + pt_bytes : s.phi + pimg_bytes;
   s.uloc_stride = static_cast<int>(align_up(p.s.rank_v, 4));
   s.uloc = s.phi;
   const uint32_t uloc_end = s.uloc + np * s.uloc_stride * 4;
@@ -920,6 +924,9 @@ FusedPlan plan_fused(const FusedShape& s) {
   if (cols > 512) return bad("TMEM budget exceeded (raise the cluster size)");
   p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   p.stages = 2;
+  p.pt_alias = false;
+  if (smem_layout(p).total > 227 * 1024 && 8u * p.np * 128 * (p.nb2 > 0 ? 2 : 1) <= 2u * p.kpk * p.np * 128)
+    p.pt_alias = true;  // large ranks (e.g. C4 2x, rank 1024): p tiles over the dead P image
   if (smem_layout(p).total > 227 * 1024) return bad("shared-memory budget exceeded");
   while (p.stages + 1 <= kMaxStages) {
     FusedPlan q = p;

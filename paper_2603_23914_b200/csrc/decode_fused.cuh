@@ -62,6 +62,7 @@ struct FusedPlan {
   int mtiles;          // vpanels / 2
   int kst;             // ring stages per tile for left_k (panel pairs)
   int nb2;             // two-tier values: U row tiles that need the second-tier accumulator
+  bool pt_alias;       // p tiles reuse the P image's shared memory (large ranks; dead after the S MMAs)
   bool stack;          // P / p hi+lo halves stacked along N (np <= 32 and TMEM allows)
   int ntiles;          // 128-token tiles per instance
   int vpanels_st;      // stored V panels (ceil(rank_v / 64))

@@ -20,6 +20,7 @@ CONFIGS = {
     "c3": dict(B=64, H=40, Hkv=40, D=128, n=4096, rk=284, rv=284, nt=64 + 128, cap=320),
     "c5": dict(B=32, H=32, Hkv=32, D=128, n=2048, rk=128, rv=128, nt=64 + 128, cap=320),
     "c4_8x": dict(B=16, H=32, Hkv=32, D=128, n=4096, rk=256, rv=256, nt=64 + 128, cap=320),
+    "c4_2x": dict(B=16, H=32, Hkv=32, D=128, n=4096, rk=1024, rv=1024, nt=64 + 128, cap=320),
 }
 
 
