@@ -253,7 +253,7 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   // diagnostics: KVP_SVD_FP32=1 forces the fp32 products, KVP_SVD_PASSES=2 two CholeskyQR passes everywhere
   const bool force_fp32 = std::getenv("KVP_SVD_FP32") != nullptr;
   const int min_passes = std::getenv("KVP_SVD_PASSES") ? std::atoi(std::getenv("KVP_SVD_PASSES")) : 1;
-  const bool tc = !precise && !force_fp32 && k <= npad && T % 8 == 0 && W % 8 == 0;
+  const bool tc = !precise && !force_fp32 && T % 8 == 0 && W % 8 == 0;
   // The range finder only needs the subspace, so its products take bf16 operands.
   // The last power-iteration product and B = Q^T A carry the factor values: they
   // use the hi/lo split (KVP_SVD_SPLIT=0 turns it off, for comparison).
@@ -280,12 +280,16 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   auto product = [&](bool trans, const float* x, bool x_batched, float* c, bool three) {
     const int xr = trans ? T : W;
     if (tc) {
-      transpose_to_bf16(x, static_cast<long>(xr) * k, xr, k, k, xt, x_batched ? batch : 1, stream);
-      range_gemm(ab, T, W, batch, trans, xt, x_batched, k, c, stream);
-      if (three) {
-        transpose_to_bf16(x, static_cast<long>(xr) * k, xr, k, k, xt_lo, x_batched ? batch : 1, stream, true);
-        range_gemm(ab, T, W, batch, trans, xt_lo, x_batched, k, c, stream, true);
-        range_gemm(ab_lo, T, W, batch, trans, xt, x_batched, k, c, stream, true);
+      // sketch columns in blocks of the kernel's 384-wide TMEM tile (k > 384: C4 4x / 2x)
+      for (int c0 = 0; c0 < k; c0 += npad) {
+        const int cw = std::min(npad, k - c0);
+        transpose_to_bf16(x + c0, static_cast<long>(xr) * k, xr, cw, k, xt, x_batched ? batch : 1, stream);
+        range_gemm(ab, T, W, batch, trans, xt, x_batched, cw, c + c0, stream, false, k);
+        if (three) {
+          transpose_to_bf16(x + c0, static_cast<long>(xr) * k, xr, cw, k, xt_lo, x_batched ? batch : 1, stream, true);
+          range_gemm(ab, T, W, batch, trans, xt_lo, x_batched, cw, c + c0, stream, true, k);
+          range_gemm(ab_lo, T, W, batch, trans, xt, x_batched, cw, c + c0, stream, true, k);
+        }
       }
     } else {
       gemm_rm(w, trans, false, trans ? W : T, k, xr, a, sA, x, x_batched ? static_cast<long>(xr) * k : 0, c,

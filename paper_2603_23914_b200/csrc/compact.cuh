@@ -14,10 +14,10 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
                             float* right, bool precise = false, float* sv = nullptr);
 // tcgen05 range-finder GEMM (compact_gemm.cu).  a: bf16 [batch][T][W];
 // xt: bf16 [batch or 1][range_gemm_npad()][K] (X^T, zero rows beyond n);
-// c: fp32 [batch][M][n] with M = trans_a ? W : T, K = trans_a ? T : W; accumulate: c += A X.
+// c: fp32 [batch][M][ldc] (ldc 0 = n) with M = trans_a ? W : T, K = trans_a ? T : W; accumulate: c += A X.
 int range_gemm_npad();
 void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, const __nv_bfloat16* xt, bool x_batched,
-                int n, float* c, cudaStream_t st, bool accumulate = false);
+                int n, float* c, cudaStream_t st, bool accumulate = false, int ldc = 0);
 // fp32 [batch][rows][cols] (row stride ld, batch stride in_stride) -> bf16 [batch][npad][rows];
 // lo: the bf16 residual x - bf16(x) instead.
 void transpose_to_bf16(const float* in, long in_stride, int rows, int cols, int ld, __nv_bfloat16* out, int batch,

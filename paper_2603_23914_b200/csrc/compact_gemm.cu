@@ -43,7 +43,7 @@ constexpr uint32_t kGSmem = kGStages * kGStage + 1024;
 template <bool TRANS_A>
 __global__ void __launch_bounds__(kGThreads, 1)
     range_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_x, int M,
-                      int K, int n, int x_batched, float* __restrict__ c, long c_stride, int accumulate) {
+                      int K, int n, int x_batched, float* __restrict__ c, long c_stride, int ldc, int accumulate) {
   extern __shared__ __align__(1024) unsigned char gsmem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsmem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[kGStages], empty[kGStages], done;
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
     mbar_wait(&done, 0);
     tc_fence_after();
     const int row = m0 + qd * 32 + lane;
-    float* crow = c + static_cast<long>(b) * c_stride + static_cast<long>(row) * n;
+    float* crow = c + static_cast<long>(b) * c_stride + static_cast<long>(row) * ldc;
     for (int c0 = 0; c0 < kNPad; c0 += 8) {
       if (c0 >= n) break;
       float v[8];
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
       if (row < M) {
         if (accumulate)
           for (int e = 0; e < 8 && c0 + e < n; ++e) v[e] += crow[c0 + e];
-        if (c0 + 8 <= n && (n & 3) == 0) {
+        if (c0 + 8 <= n && (ldc & 3) == 0) {
           *reinterpret_cast<float4*>(crow + c0) = make_float4(v[0], v[1], v[2], v[3]);
           *reinterpret_cast<float4*>(crow + c0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
         } else {
@@ -210,7 +210,8 @@ void transpose_to_bf16(const float* in, long in_stride, int rows, int cols, int 
 }
 
 void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, const __nv_bfloat16* xt,
-                bool x_batched, int n, float* c, cudaStream_t st, bool accumulate) {
+                bool x_batched, int n, float* c, cudaStream_t st, bool accumulate, int ldc) {
+  if (ldc <= 0) ldc = n;
   require(n <= kNPad, KVP_ERR_PARAMETER, "compaction: sketch width above 384 (rank + oversampling)");
   require(T % 8 == 0 && W % 8 == 0, KVP_ERR_PARAMETER, "compaction GEMM: T and W must be multiples of 8");
   const int M = trans_a ? W : T, K = trans_a ? T : W;
@@ -224,8 +225,8 @@ void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, c
     attr_set[trans_a] = true;
   }
   const dim3 grid((M + 127) / 128, batch);
-  kernel<<<grid, kGThreads, kGSmem, st>>>(ma, mx, M, K, n, x_batched ? 1 : 0, c, static_cast<long>(M) * n,
-                                          accumulate ? 1 : 0);
+  kernel<<<grid, kGThreads, kGSmem, st>>>(ma, mx, M, K, n, x_batched ? 1 : 0, c, static_cast<long>(M) * ldc,
+                                          ldc, accumulate ? 1 : 0);
   KVP_LAUNCHED();
 }
 
