@@ -669,7 +669,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) part_m[cw * NP + gbase + c0 + e] = m;
       }
     }
-    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 6] = global_ns();
     named_bar(kBarCompute, kComputeThreads);
     if (tid < H) {
       const int h = tid, w0 = (h / gcols) * 4;
@@ -770,6 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       f_me[h] = (m_loc[h] == -INFINITY ? 0.f : __expf(m_loc[h] - mg)) * zi;
     }
     named_bar(kBarCompute, kComputeThreads);
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 6] = global_ns();  // cluster statistics in hand
 
     // ---- head-averaged attention + importance EMA (importance.cpp:33-65); S re-read
     //      from TMEM concurrently with the U MMAs (disjoint TMEM columns)
@@ -820,6 +820,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     // ---- U readback (TMEM -> U_loc[h][r]); publish U_loc to the cluster
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 15] = global_ns();  // EMA + tail work done
     mbar_wait(&bars[kUFull], 0);
     tc_fence_after();
     if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 4] = global_ns();

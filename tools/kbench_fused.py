@@ -86,11 +86,11 @@ def main():
         capi.lib().kvp_debug_fused_trace(None)
         capi.lib().kvp_debug_fused_max_clusters.argtypes = [C.POINTER(FusedDesc)]
         print("max active clusters:", capi.lib().kvp_debug_fused_max_clusters(C.byref(layers[0]["desc"])))
-        t = buf.view(B * cl, 16)[:, :15].double().cpu()
+        t = buf.view(B * cl, 16)[:, :16].double().cpu()
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
-        names = ["start", "S ready", "local stats", "p tiles", "U ready", "end", "stats tmem", "mma U issued",
-                 "mma P ok", "mma S done", "prod LV0", "mma p0 ok", "mma p1 ok", "mma p2 ok", "prod last"]
+        names = ["start", "S ready", "local stats", "p tiles", "U ready", "end", "cluster stats", "mma U issued",
+                 "mma P ok", "mma S done", "prod LV0", "mma p0 ok", "mma p1 ok", "mma p2 ok", "prod last", "EMA done"]
         rel = (t - t0) / 1000.0
         print("phase (us since first CTA start): median / max over CTAs")
         for k, n_ in enumerate(names):
