@@ -154,6 +154,11 @@ int kvp_truncated_svd(const float* a, int32_t batch, int32_t T, int32_t W, int32
                       uint64_t seed, int32_t oversampling, int32_t power_iterations, float* left, float* right,
                       float* sv, void* stream);
 
+/* gaussian_matrix (linalg.hpp:55-58): rows x cols N(0,1) draws of the Philox
+ * stream (seed, stream_id) (rng.hpp:15-98), row-major, dtype f32 or f64 [dev]. */
+int kvp_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream_id, int32_t dtype, void* out,
+                        void* stream);
+
 /* ------------------------------------------------------------------------ */
 /* Fused serving kernel: bf16 compressed cache, T_q = 1, batched instances.  */
 /* ------------------------------------------------------------------------ */

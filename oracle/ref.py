@@ -120,6 +120,20 @@ class RefCache:
     def compress_now(self, decode_ini=None):
         _check(lib().kvref_compress_now(C.c_void_p(self._h), _ini(decode_ini)))
 
+    def factor_tail(self, modality, k_factors, v_factors):
+        """Install (left, right) factors (or None = dense) as the segment's joint
+        block in place of its tail (kvref_factor_tail)."""
+        args = []
+        for fac in (k_factors, v_factors):
+            if fac is None:
+                args += [C.c_size_t(0), None, None]
+            else:
+                left, right = _f64(fac[0]), _f64(fac[1])
+                args += [C.c_size_t(left.shape[1]), _dp(left), _dp(right)]
+                self._keep = getattr(self, "_keep", []) + [left, right]
+        _check(lib().kvref_factor_tail(C.c_void_p(self._h), modality, *args))
+        self._keep = []
+
     def decode_step(self, x, wq, wk, wv, wo, decode_ini=None):
         x = _f64(np.atleast_2d(x))
         out = np.zeros((x.shape[0], self.HD))

@@ -173,6 +173,38 @@ int kvref_decode_step(void* h, const char* ini, std::size_t tq, const double* x,
     });
 }
 
+// Test hook: turn the segment's tail into its single joint block with the
+// given factors instead of an SVD (what recompress_segment, decoder.cpp:455-497,
+// stores after compress_segment), so the reference can be driven on the exact
+// factors a GPU path holds.  rank 0 keeps that kind dense (the tail rows).
+// k_left: tokens x rank_k, k_right: rank_k x width (likewise v).
+int kvref_factor_tail(void* h, int modality, std::size_t rank_k, const double* k_left,
+                      const double* k_right, std::size_t rank_v, const double* v_left,
+                      const double* v_right) {
+    return guarded([&] {
+        with_cache(h, [&](auto& c) {
+            using T = typename scalar_of<std::decay_t<decltype(c)>>::type;
+            auto& seg = c.segment(mod(modality));
+            if (!seg.blocks.empty()) throw parameter_error("kvref_factor_tail: segment already has blocks");
+            const std::size_t n = seg.tail_len(), w = c.geometry.cache_width();
+            if (n == 0) throw parameter_error("kvref_factor_tail: empty tail");
+            CompressedBlock<T> block;
+            block.positions = seg.tail_positions;
+            auto store = [&](std::size_t rank, const double* l, const double* r,
+                             const Matrix<T>& rows) -> BlockStore<T> {
+                if (rank == 0) return DenseStore<T>{rows};
+                return LowRankStore<T>{FactorPair<T>{mat_in<T>(n, rank, l), mat_in<T>(rank, w, r)}};
+            };
+            block.keys = store(rank_k, k_left, k_right, seg.tail_k);
+            block.values = store(rank_v, v_left, v_right, seg.tail_v);
+            seg.blocks.push_back(std::move(block));
+            seg.tail_k = Matrix<T>(0, w);
+            seg.tail_v = Matrix<T>(0, w);
+            seg.tail_positions.clear();
+        });
+    });
+}
+
 // Plan size for the cache under `ini` (so the caller can size buffers).
 int kvref_plan_size(void* h, const char* ini, std::size_t* n) {
     return guarded([&] {

@@ -123,6 +123,8 @@ SIGNATURES = {
     "kvp_pack_left": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
     "kvp_truncated_svd": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
                                     C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "kvp_gaussian_matrix": (C.c_int, [C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_int32, C.c_void_p,
+                                      C.c_void_p]),
     "kvp_decode_fused": (C.c_int, [C.POINTER(FusedDesc), C.c_void_p]),
     "kvp_decode_fused_workspace": (C.c_size_t, [C.POINTER(FusedDesc)]),
     "kvp_engine_create": (C.c_int, [C.POINTER(EngineConfig), C.POINTER(C.c_void_p)]),

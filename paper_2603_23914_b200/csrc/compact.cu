@@ -24,6 +24,7 @@
 #include <cusolverDn.h>
 
 #include <cstdlib>
+#include <mutex>
 
 #include <algorithm>
 #include <cmath>
@@ -88,22 +89,73 @@ __global__ void f64_to_f32_kernel(const double* in, float* out, long n) {
 
 // From the ascending eigen-decomposition of C (k x k, column-major, eigvecs in
 // columns): Us[:, j] = U[:, k-1-j] * s_j and Ui[:, j] = U[:, k-1-j] / s_j for
-// the top R (descending) — fp32 column-major k x R.
+// the top R (descending) — fp32 column-major k x R.  Components below the
+// numerical rank (s_j <= kRankTol * s_max) get Us = Ui = 0: their rows of
+// `right` are filled with an orthonormal complement afterwards.
+constexpr double kRankTol = 1e-6;
 __global__ void ritz_kernel(const double* evec, const double* eval, int k, int R, float* us, float* ui, float* sv) {
   const int m = blockIdx.x;
   const double* U = evec + static_cast<long>(m) * k * k;
   const double* w = eval + static_cast<long>(m) * k;
-  const double top = fmax(w[k - 1], 0.0);
+  const double top = sqrt(fmax(w[k - 1], 0.0));
   for (int idx = threadIdx.x; idx < k * R; idx += blockDim.x) {
     const int j = idx / k, i = idx % k;
     const int src = k - 1 - j;
-    const double lam = fmax(w[src], 0.0);
-    const double s = sqrt(lam);
-    const double inv = (lam > top * 1e-28 && s > 0.0) ? 1.0 / s : 0.0;
+    const double s = sqrt(fmax(w[src], 0.0));
+    const bool live = s > kRankTol * top && s > 0.0;
     const double u = U[static_cast<long>(src) * k + i];
-    us[static_cast<long>(m) * k * R + static_cast<long>(j) * k + i] = static_cast<float>(u * s);
-    ui[static_cast<long>(m) * k * R + static_cast<long>(j) * k + i] = static_cast<float>(u * inv);
+    us[static_cast<long>(m) * k * R + static_cast<long>(j) * k + i] = live ? static_cast<float>(u * s) : 0.f;
+    ui[static_cast<long>(m) * k * R + static_cast<long>(j) * k + i] = live ? static_cast<float>(u / s) : 0.f;
     if (i == 0 && sv) sv[static_cast<long>(m) * R + j] = static_cast<float>(s);
+  }
+}
+
+// Rank-deficient input (the reference keeps orthonormal rows of `right` for
+// zero singular values, so rank prefixes stay valid): every row of `right`
+// below the numerical rank becomes a Philox Gaussian row orthogonalised twice
+// (modified Gram-Schmidt) against all other rows, then normalised.  One block
+// per matrix; `sv` holds the descending singular values.
+__global__ void complement_kernel(float* right, const float* sv, int R, int W, uint64_t seed) {
+  const int m = blockIdx.x;
+  float* rt = right + static_cast<long>(m) * R * W;
+  const float* s = sv + static_cast<long>(m) * R;
+  __shared__ float red[32];
+  __shared__ float bc;
+  const float top = s[0];
+  auto block_sum = [&](float v) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      float x = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+      for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+      if (threadIdx.x == 0) bc = x;
+    }
+    __syncthreads();
+    return bc;
+  };
+  for (int j = 0; j < R; ++j) {
+    if (s[j] > kRankTol * top && s[j] > 0.f) continue;
+    float* v = rt + static_cast<long>(j) * W;
+    for (int c = threadIdx.x; c < W; c += blockDim.x)
+      v[c] = static_cast<float>(philox_gaussian(seed, 0x636f6d70ull + m, static_cast<uint64_t>(j) * W + c));
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = 0; i < R; ++i) {
+        if (i == j || (i > j && !(s[i] > kRankTol * top && s[i] > 0.f))) continue;  // later complements: not yet built
+        const float* r = rt + static_cast<long>(i) * W;
+        float d = 0.f;
+        for (int c = threadIdx.x; c < W; c += blockDim.x) d = fmaf(v[c], r[c], d);
+        d = block_sum(d);
+        for (int c = threadIdx.x; c < W; c += blockDim.x) v[c] = fmaf(-d, r[c], v[c]);
+        __syncthreads();
+      }
+    }
+    float nn = 0.f;
+    for (int c = threadIdx.x; c < W; c += blockDim.x) nn = fmaf(v[c], v[c], nn);
+    const float inv = rsqrtf(block_sum(nn));
+    for (int c = threadIdx.x; c < W; c += blockDim.x) v[c] *= inv;
+    __syncthreads();
   }
 }
 
@@ -129,11 +181,21 @@ __global__ void to_bf16_rows_kernel(const float* in, __nv_bfloat16* out, __nv_bf
 
 unsigned grid_for(long n) { return static_cast<unsigned>((n + 255) / 256); }
 
+__global__ void nonfinite_kernel(const float* a, long n, int* flag) {
+  bool bad = false;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += static_cast<long>(gridDim.x) * blockDim.x)
+    bad |= !isfinite(a[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------
 // Batched randomized SVD on row-major fp32 matrices.
 // ---------------------------------------------------------------------------
+cudaMemPool_t svd_pool();
+std::recursive_mutex& svd_mutex();
+
 struct SvdWork {
   cublasHandle_t blas = nullptr;
   cusolverDnHandle_t solver = nullptr;
@@ -143,7 +205,7 @@ struct SvdWork {
   template <typename T>
   T* get(size_t n) {
     void* p = nullptr;
-    KVP_CUDA(cudaMallocAsync(&p, n * sizeof(T), stream));
+    KVP_CUDA(cudaMallocFromPoolAsync(&p, n * sizeof(T), svd_pool(), stream));
     bufs.push_back(p);
     return static_cast<T*>(p);
   }
@@ -220,24 +282,48 @@ void orth(SvdWork& w, float*& y, float*& spare, int m, int k, int batch, int pas
 
 }  // namespace
 
+// The cuSOLVER handle is shared by every caller of the library (expensive to
+// create); calls are serialised on it, so concurrent callers never issue work
+// on each other's streams (the reference's linalg is safe to call from many
+// threads).
+std::recursive_mutex& svd_mutex() {
+  static std::recursive_mutex m;
+  return m;
+}
+
+// Compaction scratch comes from a library-owned stream-ordered pool that keeps
+// its pages mapped between calls (the process's default pool is left alone).
+cudaMemPool_t svd_pool() {
+  static cudaMemPool_t pool = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    KVP_CUDA(cudaGetDevice(&dev));
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    KVP_CUDA(cudaMemPoolCreate(&pool, &props));
+    uint64_t keep = UINT64_MAX;
+    KVP_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  });
+  return pool;
+}
+
+void svd_pool_trim() {
+  std::lock_guard<std::recursive_mutex> lock(svd_mutex());
+  cudaMemPoolTrimTo(svd_pool(), 0);
+}
+
 void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const float* a, int batch, int T, int W,
                             int rank, uint64_t seed, int oversampling, int power_iterations, float* left,
                             float* right, bool precise, float* sv) {
-  // cuSOLVER handles are expensive to create: one per process, re-bound to the stream
+  std::lock_guard<std::recursive_mutex> lock(svd_mutex());
   static cusolverDnHandle_t solver = nullptr;
   static cusolverDnParams_t params = nullptr;
   if (!solver) {
     solver_ok(cusolverDnCreate(&solver), "cusolverDnCreate");
     solver_ok(cusolverDnCreateParams(&params), "cusolverDnCreateParams");
-  }
-  {  // the per-call workspace comes from the stream-ordered pool: keep its pages mapped
-     // between calls instead of returning them at every synchronisation
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
   }
   SvdWork w;
   w.blas = blas;
@@ -336,7 +422,8 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   // left = Q (U_R s), right = (U_R / s)^T B
   float* us = w.get<float>(static_cast<size_t>(batch) * k * rank);
   float* ui = w.get<float>(static_cast<size_t>(batch) * k * rank);
-  ritz_kernel<<<batch, 256, 0, stream>>>(cd, evals, k, rank, us, ui, sv);
+  float* svw = sv ? sv : w.get<float>(static_cast<size_t>(batch) * rank);
+  ritz_kernel<<<batch, 256, 0, stream>>>(cd, evals, k, rank, us, ui, svw);
   KVP_LAUNCHED();
   // us/ui are column-major k x R == row-major R x k (rows = components).
   // left (T x R) = Q (T x k) * Us (k x R): Us row-major (k x R) is ui^T... build explicitly:
@@ -346,6 +433,9 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   // right (R x W) = Ui^T (R x k, row-major view of ui) * B (k x W), B = (B^T)^T from the row-major W x k
   gemm_rm(w, false, true, rank, W, k, ui, static_cast<long>(k) * rank, bt, static_cast<long>(k) * W, right,
           static_cast<long>(rank) * W, batch);
+  // orthonormal complement for components below the numerical rank (rank-deficient input)
+  complement_kernel<<<batch, 512, 0, stream>>>(right, svw, rank, W, seed);
+  KVP_LAUNCHED();
   (void)hws;
 }
 
@@ -369,12 +459,49 @@ extern "C" int kvp_truncated_svd(const float* a, int32_t batch, int32_t T, int32
             "truncated_svd: rank must be in [1, min(rows, cols)]");
     require(method == 0 || method == 1, KVP_ERR_PARAMETER, "truncated_svd: method must be exact (0) or randomized (1)");
     require(oversampling >= 0 && power_iterations >= 0, KVP_ERR_PARAMETER, "truncated_svd: bad randomized options");
+    std::lock_guard<std::recursive_mutex> lock(svd_mutex());
     static cublasHandle_t blas = nullptr;
     if (!blas) blas_ok(cublasCreate(&blas), "cublasCreate");
     cudaStream_t st = as_stream(stream);
+    // check_svd_input (linalg.cpp:22-23): non-finite entries are a data_error
+    {
+      Scratch flag(sizeof(int), st);
+      KVP_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), st));
+      const long n = static_cast<long>(batch) * T * W;
+      nonfinite_kernel<<<std::min<long>(cdiv(n, 256), 4096), 256, 0, st>>>(a, n, flag.as<int>());
+      KVP_LAUNCHED();
+      int bad = 0;
+      KVP_CUDA(cudaMemcpyAsync(&bad, flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      KVP_CUDA(cudaStreamSynchronize(st));
+      require(bad == 0, KVP_ERR_DATA, "truncated_svd: matrix contains non-finite values");
+    }
     blas_ok(cublasSetStream(blas, st), "cublasSetStream");
     const bool exact = method == 0;
     randomized_svd_batched(blas, st, a, batch, T, W, rank, seed, exact ? std::min(T, W) : oversampling,
                            exact ? 2 : power_iterations, left, right, exact, sv);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI: gaussian_matrix (linalg.hpp:55-58, linalg.cpp:175-182) on the device:
+// element i (row-major) is Gaussian i of the Philox stream (seed, stream_id),
+// cast to the output dtype like the reference's float instantiation.
+// ---------------------------------------------------------------------------
+extern "C" int kvp_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream_id, int32_t dtype,
+                                   void* out, void* stream) {
+  return kvp::guarded([&] {
+    using namespace kvp;
+    require(out != nullptr, KVP_ERR_PARAMETER, "gaussian_matrix: null output");
+    require(rows >= 0 && cols >= 0, KVP_ERR_PARAMETER, "gaussian_matrix: negative shape");
+    const long n = static_cast<long>(rows * cols);
+    if (n == 0) return;
+    cudaStream_t st = as_stream(stream);
+    if (dtype == KVP_F64)
+      gaussian_kernel<double><<<grid_for(n), 256, 0, st>>>(static_cast<double*>(out), n, seed, stream_id, 0, 1.0);
+    else if (dtype == KVP_F32)
+      gaussian_kernel<float><<<grid_for(n), 256, 0, st>>>(static_cast<float*>(out), n, seed, stream_id, 0, 1.0);
+    else
+      fail(KVP_ERR_PARAMETER, "gaussian_matrix: dtype must be f32 or f64");
+    KVP_LAUNCHED();
   });
 }

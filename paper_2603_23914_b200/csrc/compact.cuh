@@ -15,6 +15,8 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
 // tcgen05 range-finder GEMM (compact_gemm.cu).  a: bf16 [batch][T][W];
 // xt: bf16 [batch or 1][range_gemm_npad()][K] (X^T, zero rows beyond n);
 // c: fp32 [batch][M][ldc] (ldc 0 = n) with M = trans_a ? W : T, K = trans_a ? T : W; accumulate: c += A X.
+// Returns the compaction scratch pool's idle pages to the device.
+void svd_pool_trim();
 int range_gemm_npad();
 void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, const __nv_bfloat16* xt, bool x_batched,
                 int n, float* c, cudaStream_t st, bool accumulate = false, int ldc = 0);

@@ -277,7 +277,11 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) qdots_kernel
       *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(st, NP, p.kpk, r >> 6, h, r & 63, false)) = __float2bfloat16_rn(0.f);
       *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(st, NP, p.kpk, r >> 6, h, r & 63, true)) = __float2bfloat16_rn(0.f);
     }
-  const int nblk = (rows + 7) / 8;
+  // The appended row is this kernel's own write: the stream loop stops before it
+  // (a non-coherent ld.global.nc of data written by the same kernel is undefined) and
+  // its logits come from the fp32 source rounded to bf16, exactly the stored row.
+  const int rows_ld = a.append_kv ? rows - 1 : rows;
+  const int nblk = (rows_ld + 7) / 8;
   const int gid = warp * GPW + grp, ngroups = (kStreamThreads / 32) * GPW;
   constexpr int UNR = QD_UNROLL;  // 8-row blocks in flight per group
   for (int blk0 = gid; blk0 < nblk; blk0 += UNR * ngroups) {
@@ -288,7 +292,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) qdots_kernel
       for (int u = 0; u < 8; ++u) {
         // unconditional load of a clamped row (no select right after the load, so
         // all loads stay in flight); rows >= `rows` are discarded at emit
-        const int r = min((blk0 + ub * ngroups) * 8 + u, rows - 1);
+        const int r = min((blk0 + ub * ngroups) * 8 + u, rows_ld - 1);
         rawb[ub][u] = ldg_stream(r < rk ? rkb + static_cast<long>(r) * W : tkb + static_cast<long>(r - rk) * W);
       }
 #pragma unroll
@@ -342,7 +346,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) qdots_kernel
       const int r = r0 + j;
       const int h = g * PER_KV + y;
       const bool owner = (gl < 8 * (LPH / 8)) && ((gl % (LPH / 8)) == 0);
-      if (owner && r < rows) {
+      if (owner && r < rows_ld) {
         if (r < rk) {
           __nv_bfloat16 hi, lo;
           split_bf16(acc[0], hi, lo);
@@ -353,6 +357,21 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) qdots_kernel
         }
       }
     }
+    }
+  }
+  if (a.append_kv && gid == ngroups - 1) {  // the appended row (tail row n_tail - 1), one lane group
+    const float* src = a.q + static_cast<long>(b) * a.q_stride + static_cast<long>(H) * D + g * D + gl * 8;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = __bfloat162float(__float2bfloat16_rn(src[e]));
+#pragma unroll
+    for (int y = 0; y < PER_KV; ++y) {
+      float t = v[0] * qv[y][0];
+#pragma unroll
+      for (int e = 1; e < 8; ++e) t = fmaf(v[e], qv[y][e], t);
+#pragma unroll
+      for (int o = LPH / 2; o >= 1; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (gl == 0) tout[static_cast<long>(g * PER_KV + y) * p.s.tail_cap + (n_tail - 1)] = t;
     }
   }
 }
@@ -457,36 +476,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int H = p.s.H;
   constexpr int NP = NPT;
   const int n_tail = a.n_tail_dev ? *a.n_tail_dev : a.n_tail;
-  if (b >= p.s.batch) {
-    // Prefetch clusters (on SMs the instance clusters leave idle): pull vsum's operands
-    // (right_v, and the tail_v rows in use) into L2 while the instances run, so the
-    // value-basis pass that follows streams from L2.  Whole clusters take this branch.
-    if (threadIdx.x < 32) {
-      const int nb = (gridDim.x / C - p.s.batch) * C, k = (b - p.s.batch) * C + c;  // prefetch CTA k of nb
-      const long W = static_cast<long>(p.s.Hkv) * p.s.D;
-      const long rv_bytes = static_cast<long>(p.s.batch) * p.s.rank_v * W * 2;
-      const long tv_bytes = static_cast<long>(n_tail) * W * 2;  // per instance (rows 0..n_tail)
-      const long total = rv_bytes + static_cast<long>(p.s.batch) * tv_bytes;
-      constexpr long kChunk = 32768;
-      const long chunks = (total + kChunk - 1) / kChunk;
-      for (long q = static_cast<long>(k) * 32 + threadIdx.x; q < chunks; q += static_cast<long>(nb) * 32) {
-        long off = q * kChunk;
-        const unsigned char* src;
-        long avail;
-        if (off < rv_bytes) {
-          src = reinterpret_cast<const unsigned char*>(a.right_v) + off;
-          avail = rv_bytes - off;
-        } else {
-          off -= rv_bytes;
-          const long inst = off / tv_bytes, o = off % tv_bytes;
-          src = reinterpret_cast<const unsigned char*>(a.tail_v) + inst * p.s.tail_cap * W * 2 + o;
-          avail = tv_bytes - o;
-        }
-        bulk_prefetch_l2(src, static_cast<uint32_t>(min(kChunk, avail)) & ~15u);
-      }
-    }
-    return;
-  }
   const Items it = make_items(p, c, n_tail);
   const uint32_t s_cols = static_cast<uint32_t>(p.max_tiles * NPW);
   const int NS = p.stages;
@@ -935,12 +924,6 @@ FusedPlan plan_fused(const FusedShape& s) {
     if (smem_layout(q).total > 227 * 1024) break;
     p.stages = q.stages;
   }
-  if (const char* e = std::getenv("KVP_FUSED_STAGES")) {  // tuning override
-    const int want = std::atoi(e);
-    if (want >= 2 && want <= kMaxStages && want < p.stages) p.stages = want;
-  }
-  p.box32_only = std::getenv("KVP_FUSED_BOX32") != nullptr;
-  if (const char* e = std::getenv("KVP_FUSED_DEBUG")) p.debug = std::atoi(e);  // timing experiments only
   p.smem_bytes = smem_layout(p).total;
   const size_t vs = (static_cast<size_t>(per_kv) * ((s.rank_v + s.tail_cap + 3) & ~3) + kStreamWarps * (256 / s.D) * per_kv * s.D) * 4;
   if (vs > 200 * 1024) return bad("vsum weights exceed shared memory");
@@ -1026,33 +1009,11 @@ void launch_vsum(const FusedPlan& p, const FusedArgs& a, cudaStream_t st) { laun
 
 int max_active_clusters(const FusedPlan& p);
 
-// Extra clusters that only prefetch vsum's operands into L2, on the SMs a
-// single wave of instance clusters leaves idle.  Off by default: measured on
-// B200 (C2: 59.6 -> 63.0 us per layer) the prefetch traffic competes with the
-// core's own streams.  KVP_PF_CLUSTERS=-1 sizes them automatically, N forces N.
-int prefetch_clusters(const FusedPlan& p) {
-  static std::map<std::tuple<int, int, int, int, int>, int> cache;
-  const auto key = std::make_tuple(p.s.batch, p.s.cluster, p.np, static_cast<int>(p.smem_bytes), p.s.rank_v);
-  const char* e = std::getenv("KVP_PF_CLUSTERS");
-  if (e == nullptr) return 0;
-  if (std::atoi(e) >= 0) return std::atoi(e);
-  if (auto f = cache.find(key); f != cache.end()) return f->second;
-  int pf = 0;
-  try {
-    const int act = max_active_clusters(p);
-    if (act > p.s.batch) pf = std::min(act - p.s.batch, 8);
-  } catch (...) {
-    pf = 0;
-  }
-  cache[key] = pf;
-  return pf;
-}
-
 void launch_core(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, int priority) {
   auto kernel = core_for(p.np, p.stack);
   KVP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_bytes)));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>((p.s.batch + prefetch_clusters(p)) * p.s.cluster));
+  cfg.gridDim = dim3(static_cast<unsigned>(p.s.batch * p.s.cluster));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = p.smem_bytes;
   cfg.stream = st;

@@ -71,8 +71,6 @@ struct FusedPlan {
   int tail_max;        // max tail tokens per CTA
   int heads_per_cta;   // query heads per CTA in the U reduce-scatter
   int stages;          // TMA ring stages (even)
-  bool box32_only;     // tuning: force 32-row TMA boxes
-  int debug;           // timing experiments (1: skip the lo-half MMAs — wrong numerics)
   size_t smem_bytes;
   int tmem_cols;
   bool ok;

@@ -57,12 +57,7 @@ struct kvp_engine {
   double tier_ratio = 0.0;
   unsigned char* vtier = nullptr;
   size_t fused_ws_bytes = 0;
-  kvp::FusedPlan plan{};   // whole batch (workspace, tensor maps)
-  kvp::FusedPlan gplan{};  // one instance group (launch grids)
-  int groups = 1;          // instance groups pipelined across two streams
-  int core_priority = 0;
-  cudaStream_t stream2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_q0 = nullptr, ev_join = nullptr;
+  kvp::FusedPlan plan{};   // whole batch
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   double compaction_ms = 0.0;  // SVD + packing of every layer (set by compact_visual)
@@ -89,9 +84,6 @@ struct kvp_engine {
         if (l) cublasLtMatrixLayoutDestroy(l);
     }
     if (lt) cublasLtDestroy(lt);
-    for (cudaEvent_t ev : {ev_fork, ev_q0, ev_join})
-      if (ev) cudaEventDestroy(ev);
-    if (stream2) cudaStreamDestroy(stream2);
     if (stream) cudaStreamDestroy(stream);
   }
   size_t lk_bytes() const { return kvp::packed_left_bytes(B, n, rk); }  // per layer, packed
@@ -264,7 +256,7 @@ void gemm_bf16(kvp_engine* e, int m, int n, int k, const __nv_bfloat16* a, const
              "cublasGemmEx");
 }
 
-FusedArgs fused_args(kvp_engine* e, int l) {
+FusedArgs fused_args(kvp_engine* e, int l, bool append_kv) {
   FusedArgs a{};
   const size_t lidx = static_cast<size_t>(l);
   a.left_k_packed = e->lk + lidx * e->lk_bytes();
@@ -277,7 +269,7 @@ FusedArgs fused_args(kvp_engine* e, int l) {
   a.n_tail = 0;
   a.q = e->qkv;  // [q | k | v] rows straight from the projection GEMM
   a.q_stride = static_cast<long>(e->HD) + 2L * e->W;
-  a.append_kv = 1;  // qdots appends k, v to the tail and zeroes the new importance
+  a.append_kv = append_kv ? 1 : 0;  // qdots appends k, v to the tail and zeroes the new importance
   a.inst0 = 0;
   a.importance = e->imp + lidx * e->B * e->imp_stride();
   a.imp_stride = static_cast<long>(e->imp_stride());
@@ -294,35 +286,14 @@ FusedArgs fused_args(kvp_engine* e, int l) {
   return a;
 }
 
-// Attention for one layer, instance groups pipelined over two streams:
-// qdots(g0) -> [core(g0) || qdots(g1)] -> [vsum(g0) || core(g1)] -> vsum(g1).
-void enqueue_attention(kvp_engine* e, int l) {
+// Attention for one layer: qdots -> cluster core -> vsum (PDL-chained).
+// append_kv = 0 leaves the cache untouched apart from the importance EMA (timing replays).
+void enqueue_attention(kvp_engine* e, int l, bool append_kv = true) {
   cudaStream_t s = e->stream;
-  const FusedArgs full = fused_args(e, l);
-  if (e->groups == 1) {
-    launch_qdots(e->gplan, full, s);
-    launch_core(e->gplan, full, s, e->core_priority);
-    launch_vsum(e->gplan, full, s);
-    return;
-  }
-  const int gb = e->gplan.s.batch;
-  KVP_CUDA(cudaEventRecord(e->ev_fork, s));
-  KVP_CUDA(cudaStreamWaitEvent(e->stream2, e->ev_fork, 0));
-  const FusedArgs a0 = offset_args(e->plan, full, 0);
-  launch_qdots(e->gplan, a0, s);
-  KVP_CUDA(cudaEventRecord(e->ev_q0, s));
-  launch_core(e->gplan, a0, s, e->core_priority);
-  launch_vsum(e->gplan, a0, s);
-  for (int g = 1; g < e->groups; ++g) {
-    const FusedArgs ag = offset_args(e->plan, full, g * gb);
-    KVP_CUDA(cudaStreamWaitEvent(e->stream2, e->ev_q0, 0));
-    launch_qdots(e->gplan, ag, e->stream2);
-    KVP_CUDA(cudaEventRecord(e->ev_q0, e->stream2));
-    launch_core(e->gplan, ag, e->stream2, e->core_priority);
-    launch_vsum(e->gplan, ag, e->stream2);
-  }
-  KVP_CUDA(cudaEventRecord(e->ev_join, e->stream2));
-  KVP_CUDA(cudaStreamWaitEvent(s, e->ev_join, 0));
+  const FusedArgs a = fused_args(e, l, append_kv);
+  launch_qdots(e->plan, a, s);
+  launch_core(e->plan, a, s, 0);
+  launch_vsum(e->plan, a, s);
 }
 
 // resolve_tiering (decoder.cpp:105-139) for the next step of every layer: assign_groups
@@ -442,7 +413,6 @@ void compact_visual(kvp_engine* e) {
   KVP_CUDA(cudaMallocAsync(&left, sizeof(float) * nb * T * rmax, s));
   KVP_CUDA(cudaMallocAsync(&right, sizeof(float) * nb * rmax * W, s));
   KVP_CUDA(cudaMallocAsync(&lb, sizeof(__nv_bfloat16) * nb * T * rmax, s));
-  require(e->rk == e->rv, KVP_ERR_PARAMETER, "engine compaction: rank_k must equal rank_v");
   const int R = e->rk;
   // compaction time = the SVD + packing only (the synthetic K/V generation is excluded)
   std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(e->L));
@@ -450,8 +420,11 @@ void compact_visual(kvp_engine* e) {
   for (int l = 0; l < e->L; ++l) {
     generate_visual(e, l, a, zbuf, lbuf);
     KVP_CUDA(cudaEventRecord(ev[2 * l], s));
-    randomized_svd_batched(e->blas, s, a, nb, T, W, R, e->cfg.svd_seed, e->cfg.svd_oversampling,
-                           e->cfg.svd_power_iterations, left, right);
+    // SvdOptions.method (linalg.hpp:12-19): exact = full sketch with fp32 products (as kvp_truncated_svd)
+    const bool exact = e->cfg.svd_method == 0;
+    randomized_svd_batched(e->blas, s, a, nb, T, W, R, e->cfg.svd_seed,
+                           exact ? std::min(T, W) : e->cfg.svd_oversampling,
+                           exact ? 2 : e->cfg.svd_power_iterations, left, right, exact);
     // split K (even) / V (odd) matrices into the layer's buffers
     for (int kind = 0; kind < 2; ++kind) {
       for (int b = 0; b < e->B; ++b) {
@@ -490,6 +463,7 @@ void compact_visual(kvp_engine* e) {
   cudaMemPool_t pool;
   if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
     cudaMemPoolTrimTo(pool, 0);
+  svd_pool_trim();
 }
 
 namespace {
@@ -527,6 +501,12 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     require(c->visual_tokens >= 1 && c->rank_k >= 1 && c->rank_v >= 1, KVP_ERR_PARAMETER,
             "engine: the serving layout needs a factored visual segment");
     require(c->alpha >= 0.0 && c->alpha <= 1.0, KVP_ERR_PARAMETER, "DecodeConfig: alpha must be in [0, 1]");
+    require(c->svd_method == 0 || c->svd_method == 1, KVP_ERR_PARAMETER,
+            "SvdOptions: method must be exact (0) or randomized (1)");
+    require(c->svd_oversampling >= 0 && c->svd_power_iterations >= 0, KVP_ERR_PARAMETER,
+            "SvdOptions: oversampling and power_iterations must be >= 0");
+    require(c->factor_init != 0 || c->rank_k == c->rank_v, KVP_ERR_PARAMETER,
+            "engine compaction: rank_k must equal rank_v (one batched SVD per layer)");
     auto e = std::make_unique<kvp_engine>();
     e->cfg = *c;
     e->H = c->heads;
@@ -558,20 +538,7 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     if (fs.cluster <= 0) fs.cluster = auto_cluster_size(fs);
     e->plan = plan_fused(fs);
     require(e->plan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->plan.why).c_str());
-    e->groups = 1;  // two-group pipelining measured slower on B200 (KVP_GROUPS to override)
-    if (const char* g = std::getenv("KVP_GROUPS")) e->groups = std::max(1, std::atoi(g));
-    require(e->B % e->groups == 0, KVP_ERR_PARAMETER, "engine: batch must divide into the instance groups");
-    FusedShape gs = fs;
-    gs.batch = e->B / e->groups;
-    e->gplan = plan_fused(gs);
-    require(e->gplan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->gplan.why).c_str());
-    int lo = 0, hi = 0;
-    KVP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    e->core_priority = hi;  // numerically lowest = highest priority
     KVP_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-    KVP_CUDA(cudaStreamCreateWithFlags(&e->stream2, cudaStreamNonBlocking));
-    for (cudaEvent_t* ev : {&e->ev_fork, &e->ev_q0, &e->ev_join})
-      KVP_CUDA(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     blas_check(cublasCreate(&e->blas), "cublasCreate");
     blas_check(cublasSetStream(e->blas, e->stream), "cublasSetStream");
     e->blas_ws = e->alloc<char>(kBlasWs);
@@ -596,7 +563,7 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     e->n_tail_dev = e->alloc<int>(1);
     e->fused_ws_bytes = fused_workspace_bytes(fs);
     e->fused_ws = e->alloc<char>(e->fused_ws_bytes);
-    if (!(std::getenv("KVP_LT") && std::atoi(std::getenv("KVP_LT")) == 0)) {
+    {
       const int nqkv = e->HD + 2 * e->W;
       lt_setup(e.get(), e->g_qkv, e->B, nqkv, e->HD, false, e->xb, e->wqkv, e->qkv);
       lt_setup(e.get(), e->g_o, e->B, e->HD, e->HD, true, e->ctx, e->wo, e->xb);
@@ -787,7 +754,8 @@ extern "C" int kvp_engine_layer_state(kvp_engine* e, int layer, kvp_engine_layer
 
 // Attention-only timing (the roofline numerator): qdots + core + vsum for
 // every layer at the current tail length, captured as a graph and replayed
-// `iters` times, CUDA events on the engine stream.  Mutates importance only.
+// `iters` times, CUDA events on the engine stream.  No token is appended
+// (append_kv = 0); the replays apply the importance EMA only.
 extern "C" int kvp_engine_time_attention(kvp_engine* e, int32_t iters, double* ms_per_layer,
                                          double* bytes_per_layer) {
   return guarded([&] {
@@ -796,7 +764,7 @@ extern "C" int kvp_engine_time_attention(kvp_engine* e, int32_t iters, double* m
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;
     KVP_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-    for (int l = 0; l < e->L; ++l) enqueue_attention(e, l);
+    for (int l = 0; l < e->L; ++l) enqueue_attention(e, l, /*append_kv=*/false);
     KVP_CUDA(cudaStreamEndCapture(s, &g));
     KVP_CUDA(cudaGraphInstantiate(&ge, g, 0));
     KVP_CUDA(cudaGraphLaunch(ge, s));  // warm-up

@@ -69,3 +69,91 @@ def attend_on_gpu(st, plan, queries, qpos, dtype="f64", with_table=True):
     torch.cuda.synchronize()
     del keep
     return ctx.cpu().numpy(), ha.cpu().numpy(), hat.cpu().numpy()[:, :tsize]
+
+
+# ---------------------------------------------------------------------------
+# Fused serving kernel (kvp_decode_fused) helpers: a synthetic bf16 serving
+# cache, the fp64 dense oracle over the same rounded factors, and one call.
+# ---------------------------------------------------------------------------
+from paper_2603_23914_b200._capi import FusedDesc  # noqa: E402
+
+
+def bf16_round(x):
+    import torch
+    return torch.as_tensor(x, dtype=torch.float32).to(torch.bfloat16).to(torch.float64).numpy()
+
+
+def make_case(rng, B, H, Hkv, D, n, rk, rv, nt, cap):
+    W = Hkv * D
+    def orth(r):
+        q, _ = np.linalg.qr(rng.standard_normal((W, r)))
+        return q.T
+    case = dict(
+        left_k=bf16_round(rng.standard_normal((B, n, rk)) * np.linspace(3, 0.3, rk)),
+        left_v=bf16_round(rng.standard_normal((B, n, rv)) * np.linspace(3, 0.3, rv)),
+        right_k=bf16_round(np.stack([orth(rk) for _ in range(B)])),
+        right_v=bf16_round(np.stack([orth(rv) for _ in range(B)])),
+        tail_k=bf16_round(rng.standard_normal((B, cap, W))),
+        tail_v=bf16_round(rng.standard_normal((B, cap, W))),
+        q=rng.standard_normal((B, H * D)).astype(np.float32).astype(np.float64) * 2.0,
+        imp=rng.uniform(0, 1, (B, n + cap)),
+    )
+    return case
+
+
+def oracle(case, H, Hkv, D, nt, alpha, tier=None, rv2=0):
+    B, n, _ = case["left_k"].shape
+    per = H // Hkv
+    ctx = np.zeros((B, H * D))
+    ha = np.zeros((B, n + nt))
+    imp = case["imp"].copy()
+    for b in range(B):
+        K = np.concatenate([case["left_k"][b] @ case["right_k"][b], case["tail_k"][b, :nt]])
+        Vc = case["left_v"][b] @ case["right_v"][b]
+        if tier is not None:  # second-tier tokens: value-rank prefix rv2 (store_decompress_row, cache.cpp:63-101)
+            t2 = tier[b] != 0
+            Vc[t2] = case["left_v"][b][t2, :rv2] @ case["right_v"][b][:rv2]
+        V = np.concatenate([Vc, case["tail_v"][b, :nt]])
+        for h in range(H):
+            g = h // per
+            s = K[:, g * D:(g + 1) * D] @ case["q"][b, h * D:(h + 1) * D] / np.sqrt(D)
+            e = np.exp(s - s.max())
+            z = e.sum()
+            ctx[b, h * D:(h + 1) * D] = e @ V[:, g * D:(g + 1) * D] / z
+            ha[b] += e / z / H
+        cols = np.r_[np.arange(n), n + np.arange(nt)]
+        imp[b, cols] = alpha * imp[b, cols] + (1 - alpha) * ha[b]
+    return ctx, ha, imp
+
+
+def run_fused(case, H, Hkv, D, nt, alpha, cluster=0, ld_pad=8, tier=None, rv2=0):
+    import torch
+    from paper_2603_23914_b200 import _capi as capi
+    B, n, rk = case["left_k"].shape
+    rv = case["left_v"].shape[2]
+    cap = case["tail_k"].shape[1]
+    def left(x):  # row-major bf16 -> packed panel-major layout (kvp_pack_left)
+        src = torch.as_tensor(x).to(torch.bfloat16).cuda().contiguous()
+        r = x.shape[2]
+        out = torch.zeros(capi.lib().kvp_packed_left_bytes(B, n, r), dtype=torch.uint8, device="cuda")
+        capi.call("kvp_pack_left", src.data_ptr(), r, B, n, r, out.data_ptr(), None)
+        return out
+    bf = lambda x: torch.as_tensor(x).to(torch.bfloat16).cuda().contiguous()
+    t = dict(lk=left(case["left_k"]), lv=left(case["left_v"]), rk=bf(case["right_k"]), rv=bf(case["right_v"]),
+             tk=bf(case["tail_k"]), tv=bf(case["tail_v"]), q=torch.as_tensor(case["q"], dtype=torch.float32).cuda(),
+             imp=torch.as_tensor(case["imp"]).cuda().contiguous())
+    ctx = torch.zeros((B, H * D), dtype=torch.float32, device="cuda")
+    ha = torch.zeros((B, n + cap), dtype=torch.float32, device="cuda")
+    d = FusedDesc(H, Hkv, D, B, n, rk, rv, 0, cap, nt, None, cluster, 0, t["lk"].data_ptr(), t["rk"].data_ptr(),
+                  t["lv"].data_ptr(), t["rv"].data_ptr(), t["tk"].data_ptr(), t["tv"].data_ptr(), t["q"].data_ptr(),
+                  t["imp"].data_ptr(), n + cap, alpha, ha.data_ptr(), ctx.data_ptr())
+    if tier is not None:
+        t["tier"] = torch.as_tensor(np.ascontiguousarray(tier, dtype=np.uint8)).cuda()
+        d.tier2_value_rank = rv2
+        d.value_tier = t["tier"].data_ptr()
+    capi.lib().kvp_decode_fused.argtypes = [C.POINTER(FusedDesc), C.c_void_p]
+    capi.check(capi.lib().kvp_decode_fused(C.byref(d), None))
+    torch.cuda.synchronize()
+    return ctx.cpu().numpy().astype(np.float64), ha.cpu().numpy().astype(np.float64), t["imp"].cpu().numpy()
+
+

@@ -15,6 +15,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 SPEC = dict(H=4, Hkv=4, D=64, L=2, B=2, n=96, t0=16, steps=4, rank=16, seed=11)
+# BASELINE configs[1] (C2) geometry: LLaVA-1.5-7B, 4 x 576 visual + 64 text tokens, rank 368 (1 instance x 2 layers)
+SPEC_C2 = dict(H=32, Hkv=32, D=128, L=2, B=1, n=2304, t0=64, steps=2, rank=368, seed=11)
 
 
 def _torch():
@@ -49,12 +51,12 @@ def unpack_left(raw_u8, B, n, rank):
     return vals.transpose(0, 1, 3, 2, 4).reshape(B, tiles * 128, panels * 64)[:, :n, :rank]
 
 
-def make_engine(factor_init="compaction", tier=None):
+def make_engine(factor_init="compaction", tier=None, s=SPEC):
     from paper_2603_23914_b200.engine import Engine, EngineSpec, ProfileSpec
-    s = SPEC
+    vis = ProfileSpec(24, 8, 0.9, 1e-2) if s is SPEC else ProfileSpec(2 * s["rank"], s["rank"], 0.98, 1e-2)
     spec = EngineSpec(heads=s["H"], kv_heads=s["Hkv"], head_dim=s["D"], layers=s["L"], batch=s["B"],
                       visual_tokens=s["n"], textual_tokens=s["t0"], decode_steps=s["steps"], rank_k=s["rank"],
-                      rank_v=s["rank"], seed=s["seed"], visual=ProfileSpec(24, 8, 0.9, 1e-2),
+                      rank_v=s["rank"], seed=s["seed"], visual=vis,
                       textual=ProfileSpec(6, 2, 0.9, 1e-3), factor_init=factor_init, svd_seed=3,
                       tier_ratio=tier[0] if tier else 0.0, tier_value_fraction=tier[1] if tier else 1.0)
     eng = Engine(spec)
@@ -62,9 +64,8 @@ def make_engine(factor_init="compaction", tier=None):
     return eng
 
 
-def layer_state(eng, l):
+def layer_state(eng, l, s=SPEC):
     from paper_2603_23914_b200 import _capi as capi
-    s = SPEC
     W, HD = s["Hkv"] * s["D"], s["H"] * s["D"]
     cap = s["t0"] + s["steps"]
     v = eng.layer(l)
@@ -100,7 +101,7 @@ def test_compaction_reconstructs_visual_segments():
                 # the reference's own randomized SVD (oracle/_ref) on the same matrix
                 rl, rr = ref.truncated_svd(a, s["rank"], method="randomized", seed=3)
                 ref_err = np.linalg.norm(a - rl @ rr) / np.linalg.norm(a)
-                assert err <= 1.05 * ref_err + 5e-3, (l, kn, b, err, ref_err)
+                assert err <= 1.05 * ref_err, (l, kn, b, err, ref_err)
                 gram = st[f"right_{kn}"][b] @ st[f"right_{kn}"][b].T
                 assert np.abs(gram - np.eye(s["rank"])).max() <= 2e-2
         # weights follow the reference's streams (harness.cpp:138-151)
@@ -110,32 +111,36 @@ def test_compaction_reconstructs_visual_segments():
     eng.close()
 
 
-@pytest.mark.parametrize("tier", [None, (0.5, 0.25)], ids=["untiered", "two_tier"])
-def test_decode_steps_match_reference(tier):
+CASES = [("small", SPEC, None), ("small", SPEC, (0.5, 0.25)), ("c2", SPEC_C2, None)]
+
+
+@pytest.mark.parametrize("name,s,tier", CASES, ids=["untiered", "two_tier", "c2_geometry"])
+def test_decode_steps_match_reference(name, s, tier):
     """Engine decode vs the reference decode_step (double) on the engine's own
-    bf16 factors, layer by layer, 4 steps, both instances; untiered, and with
+    bf16 factors and weights, layer by layer, every instance: untiered, with
     two-tier attention-aware value decompression (the reference's [decode.tiering]:
-    half the tokens by importance at full rank, the rest at a quarter of the value rank)."""
+    half the tokens by importance at full rank, the rest at a quarter of the value
+    rank), and at the C2 geometry (BASELINE configs[1]).  The engine rounds the
+    activations to bf16 before each projection and keeps the new K/V rows in bf16;
+    the reference chain stays fp64 — the bound is the bf16 storage bound."""
     torch = _torch()
     from oracle import ref
     from oracle.cases import decode_ini
-    s = SPEC
     H, Hkv, D, L, B = s["H"], s["Hkv"], s["D"], s["L"], s["B"]
     W, HD = Hkv * D, H * D
-    eng = make_engine(tier=tier)
-    states = [layer_state(eng, l) for l in range(L)]
+    eng = make_engine(tier=tier, s=s)
+    states = [layer_state(eng, l, s) for l in range(L)]
     tiering = ((tier[0], 1.0 - tier[0]), (1.0, 1.0), (1.0, tier[1])) if tier else None
     ini = decode_ini(ranks=(s["rank"], s["rank"], 0, 0), tiering=tiering, period=None, alpha=0.25)
-    # reference caches seeded with the engine's factors: visual block via compress_now of
-    # the exact reconstruction (rank-16 exact), textual tail verbatim
+    # reference caches holding the engine's factors as their joint visual block, textual tail verbatim
     caches = {}
     for l in range(L):
         for b in range(B):
             c = ref.RefCache(H, Hkv, D, dtype="f64")
             st = states[l]
-            c.append(0, st["left_k"][b] @ st["right_k"][b], st["left_v"][b] @ st["right_v"][b])
+            c.append(0, np.zeros((s["n"], W)), np.zeros((s["n"], W)))
+            c.factor_tail(0, (st["left_k"][b], st["right_k"][b]), (st["left_v"][b], st["right_v"][b]))
             c.append(1, st["tail_k"][b, :s["t0"]], st["tail_v"][b, :s["t0"]])
-            c.compress_now(ini)
             caches[(l, b)] = c
     rng = np.random.default_rng(7)
     xs = rng.standard_normal((s["steps"], B, HD)).astype(np.float32)
@@ -156,9 +161,10 @@ def test_decode_steps_match_reference(tier):
                 h = h[0]
             rel = np.linalg.norm(y[b] - h) / np.linalg.norm(h)
             worst = max(worst, rel)
-    assert worst <= 3e-2, worst  # bf16 activations/weights/cache vs the fp64 reference chain
+    print(f"{name} tier={tier}: worst relative output error {worst:.3e} over {s['steps']} steps")
+    assert worst <= 1.5e-2, worst  # bf16 activations/weights/cache vs the fp64 reference chain
     # bookkeeping: the tail grew by one row per step, new tokens' importance was updated
-    st = layer_state(eng, 0)
+    st = layer_state(eng, 0, s)
     assert st["n_tail"] == s["t0"] + s["steps"]
     pos, sc = caches[(0, 0)].importance()
     assert np.abs(st["imp"][0, :len(sc)] - sc).max() <= 2e-2
