@@ -9,14 +9,21 @@ data (Philox workload generator of the reference harness, random weights).
 A step = one decode step for every instance through every layer (projection
 GEMMs, tail append, compressed-cache attention + importance EMA, output GEMM),
 i.e. the reference's decode_step (decoder.cpp:555-617) for all (instance,
-layer) pairs.  `value` times steps with inputs resident in HBM; `e2e` times the
-same steps through the host-buffer C-ABI call (kvp_engine_step_host: H2D of
-the inputs, D2H of the outputs every step).  Per-step data (~10 GB) is far
-larger than L2 (126 MB), so no explicit flush is needed.
+layer) pairs.  The timed region covers the configuration's whole decode run
+(256 steps: the textual tail grows from 64 to 320 rows) from the post-prefill
+state; warm-up steps run first and the engine is reset to that state.
+`value` times the steps with inputs resident in HBM; `e2e` times the same
+steps through the host-buffer C-ABI call (kvp_engine_step_host: H2D of the
+inputs, D2H of the outputs every step).  Per-step data (~10 GB) is far larger
+than L2 (126 MB), so no explicit flush is needed.
 
-Multi-GPU: one process per GPU (torchrun), every rank runs its own batch of
-instances (weak scaling, no collective on the data path); the timed region is
-bracketed by barriers, max over ranks.
+Multi-GPU: one process per GPU.  `--gpus N` without a torchrun environment
+re-launches itself under torch.distributed.run (127.0.0.1).  Instances are
+split contiguously over ranks (paper_2603_23914_b200/shard.py): weak scaling
+by default (the config's batch per GPU), strong scaling with --global-batch
+(e.g. C3: 64 instances over 8 GPUs = 8 per GPU).  No collective on the
+per-step path; the timed region is bracketed by barriers and reduced as the
+max over ranks; final outputs are gathered to rank 0 once (NCCL).
 
 --impl reference runs the reference's own CPU decode step (oracle/_ref) on the
 host cores for the same config and metric (bounded sample, extrapolated).
@@ -26,6 +33,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import platform
 import subprocess
 import sys
 import threading
@@ -36,10 +44,10 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 CONFIGS = {
-    # name: geometry (H, Hkv, D), layers, batch, visual, textual, steps, rank
+    # name: geometry (H, Hkv, D), layers, batch per GPU, visual, textual, steps, rank
     "c2": dict(desc="LLaVA-1.5-7B all 32 layers, 4 images x 576 tokens + 64 text, batch 16/GPU, 4x compression",
                geom=(32, 32, 128), layers=32, batch=16, visual=2304, textual=64, steps=256, rank=368),
-    "c3": dict(desc="LLaVA-1.5-13B 40 layers, 16 images x 256 tokens + 64 text, batch 64/GPU, 8x compression",
+    "c3": dict(desc="LLaVA-1.5-13B 40 layers, 16 images x 256 tokens + 64 text, batch 64 (global), 8x compression",
                geom=(40, 40, 128), layers=40, batch=64, visual=4096, textual=64, steps=256, rank=284),
     "c5": dict(desc="VideoLLaVA-7B 8 frames x 256 tokens + 64 text, batch 32/GPU, rank 128, attention-aware "
                     "decompression: top 25% of tokens by importance at full rank, the rest at 1/4 of the value rank",
@@ -62,6 +70,16 @@ def load_peaks():
         if d.get("hbm_gbs"):
             return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
     return 6650.0, "fallback (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+def cpu_model():
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -134,10 +152,21 @@ class ClockSampler:
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(s[1] for s in self.samples), "reasons": sorted(reasons)}
 
 
+def relaunch_under_torchrun(n):
+    """`--gpus N` from a plain `python bench.py`: one process per GPU via
+    torch.distributed.run on 127.0.0.1 (the driver's own launch form)."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def dist_setup():
     """One process per GPU under torchrun: NCCL on a GPU box, gloo when no GPU is
-    visible (the multi-process CPU tests).  Only the barrier and the max-over-ranks
-    of the device-timed region use it: instances are sharded, no data-path collective."""
+    visible (the multi-process CPU tests)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -170,8 +199,21 @@ def max_over_ranks(x, world):
 
 
 def aggregate_throughput(world, batch_per_rank, steps, ms):
-    """Whole-job tokens/s: every rank decodes its own instances (weak scaling)."""
+    """Whole-job tokens/s when every rank decodes `batch_per_rank` instances."""
     return world * batch_per_rank * steps / (ms * 1e-3)
+
+
+def shard_plan(cfg, world, rank, global_batch=None):
+    """(global batch, this rank's [lo, hi) instance slice, scaling kind)."""
+    from paper_2603_23914_b200.shard import instance_range
+    if global_batch is None:
+        gb = cfg["batch"] * world
+        scaling = "weak"
+    else:
+        gb = global_batch
+        scaling = "strong"
+    lo, hi = instance_range(gb, world, rank)
+    return gb, lo, hi, scaling
 
 
 def cpu_reference(cfg, steps, warmup, threads=None):
@@ -187,9 +229,9 @@ def cpu_reference(cfg, steps, warmup, threads=None):
     secs = [sample.step() for _ in range(steps)]
     pair_s = sorted(secs)[len(secs) // 2]
     value = cb.tokens_per_second(pair_s, cfg["batch"], cfg["layers"], threads)
-    desc = (f"{threads} (instance, layer) caches of the {cfg['geom']} geometry, one reference decode_step each "
-            f"in parallel per timed step ({steps} steps, median {pair_s:.2f} s); extrapolated to "
-            f"{cfg['batch']}x{cfg['layers']} pairs per decode step")
+    desc = (f"{threads} (instance, layer) caches of the {cfg['geom']} geometry, one reference decode_step<float> "
+            f"each in parallel per timed step ({steps} steps, median {pair_s:.2f} s); extrapolated linearly to "
+            f"{cfg['batch']}x{cfg['layers']} pairs per decode step; CPU: {cpu_model()}")
     return value, threads, desc, pair_s
 
 
@@ -211,13 +253,13 @@ def warm_libraries(cfg):
     torch.cuda.synchronize()
 
 
-def compaction_block(cfg, info, world):
+def compaction_block(cfg, info, batch):
     """Prefill compaction against the tensor roofline: algorithmic flops
     2*T*W*k*(2q+2) per matrix, 2 matrices per (instance, layer)."""
     H, Hkv, D = cfg["geom"]
     T, W, R = cfg["visual"], Hkv * D, cfg["rank"]
     k = min(R + 8, min(T, W))
-    flops = 2.0 * T * W * k * (2 * 2 + 2) * 2 * cfg["batch"] * cfg["layers"]
+    flops = 2.0 * T * W * k * (2 * 2 + 2) * 2 * batch * cfg["layers"]
     peak, src = 1590.0, "fallback (B200_PROFILING.md)"
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -225,27 +267,38 @@ def compaction_block(cfg, info, world):
         if d.get("bf16_tflops_sustained"):
             peak, src = float(d["bf16_tflops_sustained"]), "MEASURED_PEAKS.json bf16_tflops_sustained"
     achieved = flops / (info.compaction_ms * 1e-3) / 1e12
-    return {"ms": info.compaction_ms, "matrices": 2 * cfg["batch"] * cfg["layers"], "shape": [T, W], "rank": R,
+    return {"ms": info.compaction_ms, "matrices": 2 * batch * cfg["layers"], "shape": [T, W], "rank": R,
             "sketch": k, "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak if peak else None, "peak_source": src,
-            "note": "randomized SVD + packing of every (instance, layer, K|V) visual segment, CUDA events; "
-                    "the synthetic K/V generation is excluded; cuBLAS/cuSOLVER warmed by one same-shape SVD beforehand"}
+            "note": "randomized SVD + packing of every (instance, layer, K|V) visual segment on this rank, CUDA "
+                    "events; the synthetic K/V generation is excluded; libraries warmed by one same-shape SVD"}
 
 
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed decode steps (default: the configuration's whole decode run, 256)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--global-batch", type=int, default=None,
+                    help="split this many instances contiguously over the ranks (strong scaling); default: the "
+                         "config's batch on every rank (weak scaling)")
     ap.add_argument("--factor-init", default="compaction", choices=["placeholder", "compaction"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tier", type=float, nargs=2, default=None, metavar=("R1", "VALUE_FRACTION"),
                     help="two-tier values: first-group ratio and the second group's value-rank fraction "
                          "(default: the config's; 0 1 = untiered)")
-    args = ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def main():
+    args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     cfg = dict(CONFIGS[args.config])
+    steps = args.steps if args.steps is not None else cfg["steps"]
     if args.tier is not None:
         cfg["tier"] = tuple(args.tier)
     tier = cfg.get("tier")
@@ -253,12 +306,18 @@ def main():
         tier = None
     cfg["tier"] = tier
     world, rank, local = dist_setup()
+    if args.config == "c3" and args.global_batch is None:
+        args.global_batch = cfg["batch"]  # BASELINE: batch 64 sharded over the GPUs
+    gb, lo, hi, scaling = shard_plan(cfg, world, rank, args.global_batch)
+    B = hi - lo
     H, Hkv, D = cfg["geom"]
     config_block = {"workload": args.config, "description": cfg["desc"], "heads": H, "kv_heads": Hkv, "head_dim": D,
-                    "layers": cfg["layers"], "batch_per_gpu": cfg["batch"], "global_batch": cfg["batch"] * world,
+                    "layers": cfg["layers"], "global_batch": gb, "batch_per_gpu": B,
                     "visual_tokens": cfg["visual"], "textual_tokens": cfg["textual"], "rank": cfg["rank"],
-                    "tail_tokens_at_timing": None, "l2_flush": "not needed: per-step data >> 126 MB L2",
-                    "parallelism": f"instance-sharded x{world} (no data-path collective)"}
+                    "decode_steps_timed": steps, "tail_tokens_timed": [cfg["textual"] + 1, cfg["textual"] + steps],
+                    "l2_flush": "not needed: per-step data (GBs) >> 126 MB L2",
+                    "parallelism": f"instance-sharded x{world} ({scaling} scaling, no per-step collective; "
+                                   f"one NCCL gather of outputs at the end)"}
     if tier is not None:
         config_block["tiering"] = {"ratios": [tier[0], 1.0 - tier[0]], "key_rank_fractions": [1.0, 1.0],
                                    "value_rank_fractions": [1.0, tier[1]]}
@@ -266,11 +325,11 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        steps, warmup = max(1, min(args.steps, 3)), min(args.warmup, 1)
-        value, threads, desc, pair_s = cpu_reference(cfg, steps, warmup)
-        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": steps,
+        rsteps, warmup = max(1, min(steps, 3)), min(args.warmup, 1)
+        value, threads, desc, pair_s = cpu_reference(cfg, rsteps, warmup)
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus, "steps": rsteps,
                 "warmup": warmup, "ms_per_step": 1e3 * cfg["batch"] / value, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+                "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
                 "config": config_block,
                 "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
                                  "sample": desc},
@@ -279,35 +338,45 @@ def main():
         return
 
     import torch
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py --impl b200 needs a CUDA device (the product path has no CPU fallback)")
     from paper_2603_23914_b200 import _capi
     from paper_2603_23914_b200.engine import Engine, EngineSpec, ProfileSpec
+    from paper_2603_23914_b200.shard import gather_instances
 
     torch.cuda.set_device(local)
-    total_steps = args.warmup + args.steps
-    spec = EngineSpec(heads=H, kv_heads=Hkv, head_dim=D, layers=cfg["layers"], batch=cfg["batch"],
+    spec = EngineSpec(heads=H, kv_heads=Hkv, head_dim=D, layers=cfg["layers"], batch=B,
                       visual_tokens=cfg["visual"], textual_tokens=cfg["textual"],
-                      decode_steps=max(cfg["steps"], total_steps), rank_k=cfg["rank"], rank_v=cfg["rank"],
-                      visual=ProfileSpec(2 * cfg["rank"], cfg["rank"], 0.98, 1e-2), seed=rank,
-                      factor_init=args.factor_init,
+                      decode_steps=max(steps, args.warmup), rank_k=cfg["rank"], rank_v=cfg["rank"],
+                      visual=ProfileSpec(2 * cfg["rank"], cfg["rank"], 0.98, 1e-2), seed=0,
+                      instance_offset=lo, factor_init=args.factor_init,
                       tier_ratio=tier[0] if tier else 0.0, tier_value_fraction=tier[1] if tier else 1.0)
     if args.factor_init == "compaction":
         warm_libraries(cfg)
     eng = Engine(spec)
     eng.prefill()
     info = eng.info()
-    B, HD = cfg["batch"], H * D
-    gen = torch.Generator(device="cuda").manual_seed(1234 + rank)
-    xs = torch.randn((total_steps, B, HD), device="cuda", generator=gen, dtype=torch.float32)
+    HD = H * D
+    # decode inputs per global instance (harness.cpp:169-170: N(0,1)), this rank's slice
+    gen = torch.Generator(device="cpu").manual_seed(1234)
+    xs_all = torch.randn((steps, gb, HD), generator=gen, dtype=torch.float32)
+    xs = xs_all[:, lo:hi].contiguous().cuda()
     ys = torch.empty((B, HD), device="cuda", dtype=torch.float32)
     stream = torch.cuda.current_stream()
 
-    def run_steps(lo, hi):
-        for t in range(lo, hi):
+    def run_steps(n):
+        for t in range(n):
             eng.step(xs[t].data_ptr(), ys.data_ptr(), stream.cuda_stream)
 
-    # ---- device-resident timing
-    run_steps(0, args.warmup)
+    # ---- warm-up, then back to the post-prefill state
+    run_steps(args.warmup)
     torch.cuda.synchronize()
+    eng.reset_steps()
+    # ---- attention alone at the first decode step's tail (roofline at both ends of the run)
+    att_ms0, att_bytes0 = eng.time_attention(iters=3)
+    eng.reset_steps()
+
+    # ---- device-resident timing of the whole decode run
     sampler = ClockSampler(local)
     sampler.start()
     sampler.wait_first()
@@ -316,39 +385,40 @@ def main():
     launches0 = _capi.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    run_steps(args.warmup, total_steps)
+    run_steps(steps)
     e1.record(stream)
     torch.cuda.synchronize()
     launches = _capi.launch_count() - launches0
     clocks = sampler.stop()
     barrier(world)
     ms = max_over_ranks(e0.elapsed_time(e1), world)
-    tail_at = cfg["textual"] + args.warmup + 1
-    config_block["tail_tokens_at_timing"] = [tail_at, tail_at + args.steps - 1]
-    value = aggregate_throughput(world, B, args.steps, ms)
+    value = gb * steps / (ms * 1e-3)
+    # ---- once per run: final-step outputs of every instance to rank 0 (ordered merge, harness.cpp:400-412)
+    gathered = gather_instances(ys, world, gb)
 
     # ---- roofline: the attention launches alone at the final tail length
-    att_ms, att_bytes = eng.time_attention(iters=3)
+    att_ms1, att_bytes1 = eng.time_attention(iters=3)
     peak, peak_src = load_peaks()
-    achieved = att_bytes / (att_ms * 1e-3) / 1e9
+    achieved = att_bytes1 / (att_ms1 * 1e-3) / 1e9
     traffic = None
     ncu_file = ROOT / "profiles" / f"ncu_attention_{args.config}.json"
     if ncu_file.exists():
         traffic = json.loads(ncu_file.read_text()).get("dram_bytes_per_layer")
+    # cache path (attention + EMA launches of every layer) at the mean of the run's first and last tail
+    cache_ms_step = 0.5 * (att_ms0 + att_ms1) * cfg["layers"]
+    cache_path = max_over_ranks(cache_ms_step, world)
 
-    # ---- e2e through the host-buffer C-ABI call
+    # ---- e2e through the host-buffer C-ABI call, same steps from the same state
     eng.reset_steps()
-    xh = torch.empty((total_steps, B, HD), dtype=torch.float32, pin_memory=True)
-    xh.copy_(xs.cpu())
+    xh = torch.empty((steps, B, HD), dtype=torch.float32, pin_memory=True)
+    xh.copy_(xs_all[:, lo:hi])
     yh = torch.empty((B, HD), dtype=torch.float32, pin_memory=True)
-    for t in range(args.warmup):
-        eng.step_host(xh[t].data_ptr(), yh.data_ptr())
     barrier(world)
     t0 = time.perf_counter()
-    for t in range(args.warmup, total_steps):
+    for t in range(steps):
         eng.step_host(xh[t].data_ptr(), yh.data_ptr())
     e2e_s = max_over_ranks(time.perf_counter() - t0, world)
-    e2e_value = world * B * args.steps / e2e_s
+    e2e_value = gb * steps / e2e_s
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -359,22 +429,30 @@ def main():
             cpu = {"value": None, "unit": "tokens/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {exc}"}
 
     if rank == 0:
-        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        out = gathered.double().cpu()
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": steps,
+                "warmup": args.warmup, "ms_per_step": ms / steps, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "bf16", "data": "synthetic (Philox workload generator, random weights)",
                 "config": config_block,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                              "frac": achieved / peak, "traffic": traffic,
-                             "kernel": "decode attention (qdots + cluster core + vsum) per layer",
-                             "peak_source": peak_src,
-                             "ms_per_layer": att_ms, "algorithmic_bytes_per_layer": att_bytes},
+                             "kernel": "decode attention (qdots + cluster core + vsum) per layer, final tail",
+                             "peak_source": peak_src, "tail_tokens": cfg["textual"] + steps,
+                             "ms_per_layer": att_ms1, "algorithmic_bytes_per_layer": att_bytes1,
+                             "first_step": {"ms_per_layer": att_ms0, "algorithmic_bytes_per_layer": att_bytes0,
+                                            "frac": att_bytes0 / (att_ms0 * 1e-3) / 1e9 / peak}},
+                "cache_path": {"value": gb / (cache_path * 1e-3), "unit": "tokens/s",
+                               "note": "attention + importance launches of every layer alone (no projections), "
+                                       "mean of the first and last step's tail"},
                 "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": B * HD * 4,
                         "d2h_bytes_per_step": B * HD * 4},
                 "gpu_launches": int(launches),
                 "clocks": clocks,
+                "gathered": {"instances": int(out.shape[0]), "output_l2": float(out.norm()),
+                             "output_sum": float(out.sum())},
                 "compaction_ms": info.compaction_ms if args.factor_init == "compaction" else None,
-                "compaction": compaction_block(cfg, info, world) if args.factor_init == "compaction" else None,
+                "compaction": compaction_block(cfg, info, B) if args.factor_init == "compaction" else None,
                 "factor_init": args.factor_init,
                 "cluster": info.cluster}
         print(json.dumps(line), flush=True)

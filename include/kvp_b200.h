@@ -222,6 +222,120 @@ size_t kvp_decode_fused_workspace(const kvp_fused_desc* desc);
 int kvp_decode_fused(const kvp_fused_desc* desc, void* stream);
 
 /* ------------------------------------------------------------------------ */
+/* Device LayerCache batch: the caller-owned cache of decode_step / compress_now */
+/* (cache.hpp:120-146 LayerCache, decoder.hpp:166-191).                        */
+/* ------------------------------------------------------------------------ */
+
+/* `batch` LayerCaches of one layer, held on the device and stepped together:
+ * every instance has the same segment structure (token counts, positions,
+ * block layout — what the reference harness builds for a batch of requests,
+ * harness.cpp:239-360); payloads, importance scores and stored ranks are per
+ * instance.  Storage dtype f32 / f64 (the reference's two instantiations,
+ * cache.cpp:241-242) or bf16 (the serving format).  A kvp_cache is
+ * single-writer. */
+typedef struct kvp_cache kvp_cache;
+
+typedef struct {
+  int32_t heads, kv_heads, head_dim; /* HeadGeometry (cache.hpp:21-31) */
+  int32_t dtype;                     /* storage: KVP_F32, KVP_F64 or KVP_BF16 */
+  int32_t batch;                     /* instances */
+  int32_t layer_index;               /* LayerCache.layer_index (rank schemes) */
+} kvp_cache_config;
+
+/* DecodeConfig (decoder.hpp:53-75) with TierSpec, MatrixRanks, SvdOptions and
+ * RankScheme (compressor.hpp:14-30).  Arrays are [host]. */
+typedef struct {
+  int64_t compression_period;        /* tail rows that trigger re-factorisation; <= 0 = never (nullopt) */
+  int32_t rank_key_visual, rank_value_visual, rank_key_textual, rank_value_textual; /* 0 = dense */
+  int32_t rank_scheme;               /* -1 none, 0 fixed, 1 linear_schedule, 2 variance_target */
+  int32_t scheme_fixed_rank;
+  int32_t scheme_first_layer_rank, scheme_last_layer_rank, scheme_num_layers;
+  double scheme_variance_target;
+  int32_t scheme_max_rank;
+  int32_t n_tiers;                   /* TierSpec groups, 0 = full-rank decompression */
+  const double* tier_ratios;
+  const double* tier_key_fractions;
+  const double* tier_value_fractions;
+  double alpha;                      /* importance EMA factor */
+  int32_t svd_method;                /* 0 exact, 1 randomized (linalg.hpp:12-19) */
+  uint64_t svd_seed;
+  int32_t svd_oversampling, svd_power_iterations;
+  int32_t recompress;                /* 0 joint, 1 separate_epochs (RecompressMode) */
+  int32_t bytes_per_scalar;          /* accounting width of the reports */
+} kvp_decode_config;
+
+/* StepReport (decoder.hpp:145-160), one per instance. */
+typedef struct {
+  uint64_t step, bytes_before, bytes_after, importance_bytes;
+  uint64_t decompress_flops, decompress_flops_full;
+  double flops_reduction;
+  int32_t compression_event;
+  int32_t n_warnings;                /* rank-clamp warnings (decoder.cpp:440-449) */
+} kvp_step_report;
+
+/* AttentionWeights (decoder.hpp:18-26): [dev] row-major, storage dtype;
+ * w_q, w_o: HD x HD, w_k, w_v: HD x W. */
+typedef struct {
+  const void *w_q, *w_k, *w_v, *w_o;
+} kvp_weights;
+
+/* CacheBytes (cache.hpp:158-168) of one instance. */
+typedef struct {
+  uint64_t visual_scalars, textual_scalars, visual_bytes, textual_bytes, cache_bytes, importance_bytes;
+} kvp_cache_bytes;
+
+int kvp_cache_create(const kvp_cache_config* config, kvp_cache** cache);
+int kvp_cache_destroy(kvp_cache* cache);
+/* append_tokens (cache.cpp:147-170) to every instance: k, v [host] f64,
+ * batch x n x W; fresh global positions, importance 0. */
+int kvp_cache_append(kvp_cache* cache, int32_t modality, int32_t n, const double* k, const double* v);
+/* Upload of a host LayerCache image: the segment's current tail becomes one
+ * block (appended after existing blocks) holding the given factors instead of
+ * an SVD — left: batch x n x rank, right: batch x rank x W, [host] f64; rank 0
+ * keeps that kind dense (the tail rows).  */
+int kvp_cache_factor_tail(kvp_cache* cache, int32_t modality, int32_t rank_k, const double* k_left,
+                          const double* k_right, int32_t rank_v, const double* v_left, const double* v_right);
+/* Importance table (importance.hpp:16-31): scores [host] batch x table_size. */
+int kvp_cache_set_importance(kvp_cache* cache, const double* scores);
+int kvp_cache_get_importance(kvp_cache* cache, uint64_t* positions /*table_size, nullable*/,
+                             double* scores /*batch x table_size, nullable*/);
+/* Shape: table size, next_position, steps_taken; per segment blocks and tail length. */
+int kvp_cache_shape(kvp_cache* cache, int32_t* table_size, uint64_t* next_position, uint64_t* steps_taken,
+                    int32_t* n_blocks /*[2]*/, int32_t* tail_len /*[2]*/);
+/* One block store of one instance: tokens and stored rank (0 = dense). */
+int kvp_cache_block_info(kvp_cache* cache, int32_t instance, int32_t modality, int32_t block, int32_t kind,
+                         int32_t* tokens, int32_t* rank);
+/* Download: low-rank -> left (tokens x rank) and right (rank x W); dense -> rows
+ * (tokens x W) into `left`.  [host] f64; positions: tokens (nullable). */
+int kvp_cache_block_get(kvp_cache* cache, int32_t instance, int32_t modality, int32_t block, int32_t kind,
+                        double* left, double* right, uint64_t* positions);
+int kvp_cache_tail_get(kvp_cache* cache, int32_t instance, int32_t modality, double* k, double* v,
+                       uint64_t* positions);
+/* memory_bytes (cache.cpp:209-219) of one instance. */
+int kvp_cache_memory_bytes(kvp_cache* cache, int32_t instance, int32_t bytes_per_scalar, kvp_cache_bytes* out);
+
+/* segment_full_matrix (decoder.cpp:406-424): dense [blocks at full stored rank;
+ * tail] of one segment and kind for every instance, [dev] f64 batch x T x W. */
+int kvp_segment_full_matrix(kvp_cache* cache, int32_t modality, int32_t kind, double* out, void* stream);
+
+/* compress_now (decoder.cpp:619-628): re-factorise every compressible segment
+ * with a non-empty tail (recompress_segment, decoder.cpp:455-497: joint or
+ * separate epochs, rank clamp, dense kinds) on the device.  reports [host]
+ * batch entries (nullable); compression_event / n_warnings are set. */
+int kvp_compress_now(kvp_cache* cache, const kvp_decode_config* cfg, kvp_step_report* reports, void* stream);
+
+/* decode_step (decoder.cpp:555-617) for every instance: project h (T_q rows),
+ * append the new K/V to `modality`'s tail, tier the compressed tokens by
+ * importance, attend over the plan in the low-rank space, W_o, EMA update,
+ * re-factorise segments whose tail reached the period.  h, out: [dev]
+ * batch x tq x HD, f64 for f64 caches, else f32.  Serving-shaped bf16 caches
+ * (one factored visual block, dense textual tail, T_q = 1, <= 2 value tiers)
+ * run the fused tcgen05 kernel; every other cache the generic plan kernels.
+ * Errors as the reference: non-finite h -> KVP_ERR_DATA before any change. */
+int kvp_decode_step(kvp_cache* cache, const void* h, int32_t tq, int32_t modality, const kvp_weights* weights,
+                    const kvp_decode_config* cfg, void* out, kvp_step_report* reports, void* stream);
+
+/* ------------------------------------------------------------------------ */
 /* Device decode engine: the batched serving loop of the synthetic harness   */
 /* (harness.cpp:239-360 run_instance, decoder.cpp:555-617 decode_step).      */
 /* ------------------------------------------------------------------------ */
@@ -256,6 +370,10 @@ typedef struct {
      resolved_tier_rank(tier_value_fraction, rank_v); key fractions 1.  tier_ratio 0 or fraction 1 = untiered */
   double tier_ratio;
   double tier_value_fraction;
+  /* global index of this engine's first instance: instance b draws the Philox
+     streams of instance instance_offset + b (harness.cpp:29-32), so a batch
+     sharded over ranks reproduces the single-process workload */
+  int32_t instance_offset;
 } kvp_engine_config;
 
 typedef struct {

@@ -90,7 +90,7 @@ class EngineConfig(C.Structure):
                 ("seed", C.c_uint64), ("visual", Profile), ("textual", Profile), ("svd_method", C.c_int32),
                 ("svd_seed", C.c_uint64), ("svd_oversampling", C.c_int32), ("svd_power_iterations", C.c_int32),
                 ("factor_init", C.c_int32), ("cluster", C.c_int32), ("tier_ratio", C.c_double),
-                ("tier_value_fraction", C.c_double)]
+                ("tier_value_fraction", C.c_double), ("instance_offset", C.c_int32)]
 
 
 class EngineInfo(C.Structure):
@@ -108,7 +108,56 @@ class LayerView(C.Structure):
 
 
 # name -> (restype, argtypes); every symbol include/kvp_b200.h declares.
+class CacheConfigC(C.Structure):
+    _fields_ = [("heads", C.c_int32), ("kv_heads", C.c_int32), ("head_dim", C.c_int32), ("dtype", C.c_int32),
+                ("batch", C.c_int32), ("layer_index", C.c_int32)]
+
+
+class DecodeConfigC(C.Structure):
+    _fields_ = [("compression_period", C.c_int64), ("rank_key_visual", C.c_int32), ("rank_value_visual", C.c_int32),
+                ("rank_key_textual", C.c_int32), ("rank_value_textual", C.c_int32), ("rank_scheme", C.c_int32),
+                ("scheme_fixed_rank", C.c_int32), ("scheme_first_layer_rank", C.c_int32),
+                ("scheme_last_layer_rank", C.c_int32), ("scheme_num_layers", C.c_int32),
+                ("scheme_variance_target", C.c_double), ("scheme_max_rank", C.c_int32), ("n_tiers", C.c_int32),
+                ("tier_ratios", C.POINTER(C.c_double)), ("tier_key_fractions", C.POINTER(C.c_double)),
+                ("tier_value_fractions", C.POINTER(C.c_double)), ("alpha", C.c_double), ("svd_method", C.c_int32),
+                ("svd_seed", C.c_uint64), ("svd_oversampling", C.c_int32), ("svd_power_iterations", C.c_int32),
+                ("recompress", C.c_int32), ("bytes_per_scalar", C.c_int32)]
+
+
+class StepReportC(C.Structure):
+    _fields_ = [("step", C.c_uint64), ("bytes_before", C.c_uint64), ("bytes_after", C.c_uint64),
+                ("importance_bytes", C.c_uint64), ("decompress_flops", C.c_uint64),
+                ("decompress_flops_full", C.c_uint64), ("flops_reduction", C.c_double),
+                ("compression_event", C.c_int32), ("n_warnings", C.c_int32)]
+
+
+class WeightsC(C.Structure):
+    _fields_ = [("w_q", C.c_void_p), ("w_k", C.c_void_p), ("w_v", C.c_void_p), ("w_o", C.c_void_p)]
+
+
+class CacheBytesC(C.Structure):
+    _fields_ = [("visual_scalars", C.c_uint64), ("textual_scalars", C.c_uint64), ("visual_bytes", C.c_uint64),
+                ("textual_bytes", C.c_uint64), ("cache_bytes", C.c_uint64), ("importance_bytes", C.c_uint64)]
+
+
+_P = C.c_void_p
 SIGNATURES = {
+    "kvp_cache_create": (C.c_int, [C.POINTER(CacheConfigC), C.POINTER(C.c_void_p)]),
+    "kvp_cache_destroy": (C.c_int, [_P]),
+    "kvp_cache_append": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P]),
+    "kvp_cache_factor_tail": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, C.c_int32, _P, _P]),
+    "kvp_cache_set_importance": (C.c_int, [_P, _P]),
+    "kvp_cache_get_importance": (C.c_int, [_P, _P, _P]),
+    "kvp_cache_shape": (C.c_int, [_P, _P, _P, _P, _P, _P]),
+    "kvp_cache_block_info": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P]),
+    "kvp_cache_block_get": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P]),
+    "kvp_cache_tail_get": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P]),
+    "kvp_cache_memory_bytes": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(CacheBytesC)]),
+    "kvp_segment_full_matrix": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P]),
+    "kvp_compress_now": (C.c_int, [_P, C.POINTER(DecodeConfigC), _P, _P]),
+    "kvp_decode_step": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.POINTER(WeightsC), C.POINTER(DecodeConfigC), _P,
+                                  _P, _P]),
     "kvp_abi_version": (C.c_int, []),
     "kvp_last_error_message": (C.c_char_p, []),
     "kvp_launch_count": (C.c_uint64, []),

@@ -369,7 +369,7 @@ void generate_visual(kvp_engine* e, int l, float* a, float* zbuf, float* lbuf) {
   const uint64_t seed = e->cfg.seed;
   for (int b = 0; b < e->B; ++b)
     for (int kind = 0; kind < 2; ++kind) {
-      const uint64_t st = stream_id(2, b, l, kind);
+      const uint64_t st = stream_id(2, e->cfg.instance_offset + b, l, kind);
       float* out = a + (static_cast<size_t>(b) * 2 + kind) * T * W;
       const long nz = static_cast<long>(T) * r;
       launch_1d(nz, [&](unsigned g, int t) { gauss_f32_kernel<<<g, t, 0, s>>>(zbuf, nz, seed, st, 0); });
@@ -498,6 +498,7 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
             "HeadGeometry: head counts and head_dim must be positive");
     require(c->heads % c->kv_heads == 0, KVP_ERR_PARAMETER, "HeadGeometry: num_kv_heads must divide num_query_heads");
     require(c->layers >= 1 && c->batch >= 1, KVP_ERR_PARAMETER, "WorkloadSpec: layers and batch must be >= 1");
+    require(c->instance_offset >= 0, KVP_ERR_PARAMETER, "engine: instance_offset must be >= 0");
     require(c->visual_tokens >= 1 && c->rank_k >= 1 && c->rank_v >= 1, KVP_ERR_PARAMETER,
             "engine: the serving layout needs a factored visual segment");
     require(c->alpha >= 0.0 && c->alpha <= 1.0, KVP_ERR_PARAMETER, "DecodeConfig: alpha must be in [0, 1]");
@@ -613,7 +614,7 @@ extern "C" int kvp_engine_prefill(kvp_engine* e) {
             launch_1d(static_cast<long>(e->t0) * e->W, [&](unsigned g, int t) {
               latent_direct_kernel<<<g, t, 0, s>>>(dst, e->W, e->t0, e->Hkv, e->D, pr.true_rank,
                                                    std::min(pr.shared_subspace, pr.true_rank), pr.spectrum_decay,
-                                                   pr.noise_floor, seed, stream_id(2, b, l, 2 + kind));
+                                                   pr.noise_floor, seed, stream_id(2, e->cfg.instance_offset + b, l, 2 + kind));
             });
           }
     }
@@ -634,7 +635,7 @@ extern "C" int kvp_engine_prefill(kvp_engine* e) {
                                    static_cast<size_t>(b) * rank * e->W;
             launch_1d(static_cast<long>(e->n) * rank + static_cast<long>(rank) * e->W, [&](unsigned g, int t) {
               synth_factor_kernel<<<g, t, 0, s>>>(scratch + static_cast<size_t>(b) * e->n * rank, e->n, rank, right,
-                                                  e->W, seed, stream_id(2, b, l, kind));
+                                                  e->W, seed, stream_id(2, e->cfg.instance_offset + b, l, kind));
             });
           }
           unsigned char* dst = kind == 0 ? e->lk + static_cast<size_t>(l) * e->lk_bytes()
@@ -702,6 +703,8 @@ extern "C" int kvp_engine_reset_steps(kvp_engine* e) {
   return guarded([&] {
     require(e != nullptr, KVP_ERR_PARAMETER, "engine: null");
     KVP_CUDA(cudaMemcpyAsync(e->n_tail_dev, &e->t0, sizeof(int), cudaMemcpyHostToDevice, e->stream));
+    // back to the post-prefill state: importance 0 everywhere (importance.cpp:9-14), tiers from it
+    KVP_CUDA(cudaMemsetAsync(e->imp, 0, sizeof(double) * e->L * e->B * e->imp_stride(), e->stream));
     assign_all_tiers(e, e->stream);
     KVP_CUDA(cudaStreamSynchronize(e->stream));
     e->steps_taken = 0;

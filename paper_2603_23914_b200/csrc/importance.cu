@@ -17,7 +17,7 @@
 namespace kvp {
 
 // s_j <- decay*s_j + blend*mean_t attn[t][j]; one thread per (table, j).
-__global__ void ema_kernel(int n_tables, int n, double* __restrict__ scores, int tq,
+__global__ void ema_kernel(int n_tables, int n, double* __restrict__ scores, long stride, int tq,
                            const double* __restrict__ attn, double decay, double blend, double inv_tq) {
   const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long)n_tables * n) return;
@@ -26,7 +26,8 @@ __global__ void ema_kernel(int n_tables, int n, double* __restrict__ scores, int
   double mean = 0.0;
   for (int t = 0; t < tq; ++t) mean = __dadd_rn(mean, a[(long)t * n]);
   mean = __dmul_rn(mean, inv_tq);
-  scores[idx] = __dadd_rn(__dmul_rn(decay, scores[idx]), __dmul_rn(blend, mean));
+  double* sc = scores + tbl * stride + j;
+  *sc = __dadd_rn(__dmul_rn(decay, *sc), __dmul_rn(blend, mean));
 }
 
 // |row sum - 1| > 1e-4 or non-finite -> count it (importance.cpp:45-54).
@@ -51,8 +52,13 @@ __global__ void row_check_kernel(int n, const double* __restrict__ attn, unsigne
   if (threadIdx.x == 0 && (nonfinite || fabs(red[0] - 1.0) > 1e-4)) atomicAdd(bad, 1u);
 }
 
+void launch_row_check(int rows, int n, const double* attn, unsigned* bad, cudaStream_t s) {
+  row_check_kernel<<<rows, 256, 0, s>>>(n, attn, bad);
+  KVP_LAUNCHED();
+}
+
 void launch_ema(int n_tables, int n, double* scores, int tq, const double* attn, double alpha,
-                unsigned* bad_rows, cudaStream_t s) {
+                unsigned* bad_rows, cudaStream_t s, long score_stride) {
   // decay = alpha^tq with the same libm pow the reference calls
   // (importance.cpp:58); blend and 1/tq as in importance.cpp:59-60.
   const double decay = std::pow(alpha, static_cast<double>(tq));
@@ -63,7 +69,8 @@ void launch_ema(int n_tables, int n, double* scores, int tq, const double* attn,
     KVP_LAUNCHED();
   }
   const long total = (long)n_tables * n;
-  ema_kernel<<<cdiv(total, 256), 256, 0, s>>>(n_tables, n, scores, tq, attn, decay, blend, inv_tq);
+  ema_kernel<<<cdiv(total, 256), 256, 0, s>>>(n_tables, n, scores, score_stride < 0 ? n : score_stride, tq, attn,
+                                               decay, blend, inv_tq);
   KVP_LAUNCHED();
 }
 
@@ -284,8 +291,7 @@ TierParams make_tier_params(int n, int n_groups, const double* ratios, const int
 void launch_tiers(int n_tables, int n, const double* scores, long stride, int n_groups, const TierParams& tp,
                   uint8_t* tier_out, uint16_t* rk_out, uint16_t* rv_out, cudaStream_t s) {
   if (n == 0 || n_tables == 0) return;
-  static const bool force_sort = std::getenv("KVP_TIER_SORT") != nullptr;  // A/B: the bitonic sort
-  if (n <= kSelThreads * kSelPer && !force_sort) {
+  if (n <= kSelThreads * kSelPer) {
     tier_select_kernel<<<n_tables, kSelThreads, 0, s>>>(n, scores, stride, n_groups, tp, tier_out, rk_out, rv_out);
     KVP_LAUNCHED();
     return;

@@ -45,13 +45,14 @@ class EngineSpec:
     cluster: int = 0
     tier_ratio: float = 0.0           # two-tier values: first-group ratio (0 = untiered)
     tier_value_fraction: float = 1.0  # value-rank fraction of the second group
+    instance_offset: int = 0          # global index of instance 0 (Philox streams of the sharded batch)
 
     def to_c(self) -> capi.EngineConfig:
         vis = self.visual or ProfileSpec(2 * self.rank_k, self.rank_k, 0.98, 1e-2)
         c = capi.EngineConfig()
         for k in ("heads", "kv_heads", "head_dim", "layers", "batch", "visual_tokens", "textual_tokens",
                   "decode_steps", "rank_k", "rank_v", "alpha", "seed", "svd_seed", "svd_oversampling",
-                  "svd_power_iterations", "cluster", "tier_ratio", "tier_value_fraction"):
+                  "svd_power_iterations", "cluster", "tier_ratio", "tier_value_fraction", "instance_offset"):
             setattr(c, k, getattr(self, k))
         c.visual = capi.Profile(vis.true_rank, vis.shared_subspace, vis.spectrum_decay, vis.noise_floor)
         t = self.textual
