@@ -97,7 +97,10 @@ __host__ __device__ inline Smem smem_layout(const FusedPlan& p) {
   const uint32_t uloc_end = s.uloc + np * s.uloc_stride * 4;
   s.stail = align_up(pt_end > uloc_end ? pt_end : uloc_end, 16);
   s.part = s.stail + p.tail_max * np * 4;
-  s.stats = s.part + 2 * kComputeWarps * np * 4 + 4 * 128 * 4;
+  // part: per-warp softmax partials, then (split) every peer's (m, z), then the EMA's head sums
+  const uint32_t part_bytes = 2 * kComputeWarps * np * 4 + 4 * 128 * 4;
+  const uint32_t peer_bytes = p.split ? static_cast<uint32_t>(p.s.cluster) * 2 * np * 4 : 0;
+  s.stats = s.part + (part_bytes > peer_bytes ? part_bytes : peer_bytes);
   s.imps = align_up(s.stats + (5 + 8) * np * 4, 16);
   s.bars = align_up(s.imps + (p.chunk + p.tail_max) * 8, 8);
   s.tslot = s.bars + 40 * 8;
@@ -235,6 +238,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) qdots_kernel
   const int H = p.s.H, W = p.s.Hkv * D;
   griddep_wait();               // q (and the new k, v) come from the projection GEMM
   griddep_launch_dependents();  // core may start its q-independent prologue and left_k stream
+  if (p.split && g == 0 && threadIdx.x == 0) a.ws_count[b] = 0u;  // core's per-instance barrier (after its wait)
   const int n_tail = a.n_tail_dev ? *a.n_tail_dev : a.n_tail;
   const int rk = p.s.rank_k, rows = rk + n_tail;
   const float scale = rsqrtf(static_cast<float>(D));
@@ -411,10 +415,23 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) vsum_kernel(
   // while core finishes.  The weights U / p_tail are core's output.
   issue(r0);
   griddep_wait();
-  for (int i = threadIdx.x; i < PER_KV * rows; i += kStreamThreads) {
-    const int y = i / rows, r = i % rows, h = g * PER_KV + y;
-    wts[y * wstride + r] = r < rv ? a.ws_u[(static_cast<long>(b) * H + h) * rv + r]
-                                  : a.ws_tail[(static_cast<long>(b) * H + h) * p.s.tail_cap + (r - rv)];
+  if (p.split) {  // U = sum of the token chunks' partials (each already scaled by its softmax correction)
+    const int C = p.s.cluster;
+    for (int i = threadIdx.x; i < PER_KV * rows; i += kStreamThreads) {
+      const int y = i / rows, r = i % rows, h = g * PER_KV + y;
+      float u = 0.f;
+      if (r < rv)
+        for (int cc = 0; cc < C; ++cc) u += __ldcg(&a.ws_u[((static_cast<long>(b) * C + cc) * H + h) * rv + r]);
+      else
+        u = a.ws_tail[(static_cast<long>(b) * H + h) * p.s.tail_cap + (r - rv)];
+      wts[y * wstride + r] = u;
+    }
+  } else {
+    for (int i = threadIdx.x; i < PER_KV * rows; i += kStreamThreads) {
+      const int y = i / rows, r = i % rows, h = g * PER_KV + y;
+      wts[y * wstride + r] = r < rv ? a.ws_u[(static_cast<long>(b) * H + h) * rv + r]
+                                    : a.ws_tail[(static_cast<long>(b) * H + h) * p.s.tail_cap + (r - rv)];
+    }
   }
   __syncthreads();
   float acc[PER_KV][8];
@@ -461,7 +478,11 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) vsum_kernel(
 // ============================================================================
 // 2. core: one cluster of C CTAs per instance.
 // ============================================================================
-template <int NPT, bool ST>  // ST: hi/lo stacked along N (plan.stack)
+// SPLIT: the instance's token chunks run as independent CTAs (any count, all SMs) that exchange their
+// softmax statistics through global memory behind a per-instance arrival counter, and write U partials
+// (scaled by their correction factor) for vsum to sum; otherwise one thread-block cluster per instance
+// exchanges through DSMEM and reduce-scatters U.
+template <int NPT, bool ST, bool SPLIT>  // ST: hi/lo stacked along N (plan.stack)
 __global__ void __launch_bounds__(kThreads, 1)
     core_kernel(const FusedPlan p, const FusedArgs a) {
   constexpr int NPW = ST ? 2 * NPT : NPT;      // TMEM columns of one S / U tile
@@ -471,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + L.tslot);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int C = p.s.cluster;
-  const int c = static_cast<int>(cluster_rank());
+  const int c = SPLIT ? static_cast<int>(blockIdx.x % C) : static_cast<int>(cluster_rank());
   const int b = blockIdx.x / C;
   const int H = p.s.H;
   constexpr int NP = NPT;
@@ -494,24 +515,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   fence_proxy_async();  // zeroed operand bytes visible to the async proxy
   tc_fence_before();
   __syncthreads();
-  cluster_sync();  // every CTA's barriers exist before any remote arrive
+  if (!SPLIT) cluster_sync();  // every CTA's barriers exist before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
   // Programmatic dependent launch: everything above and the first ring of left_k
   // stages is independent of qdots; qdots' outputs (P image, tail logits, the
   // appended tail row's zeroed importance) are read only after griddep_wait.
+  // Split mode triggers its dependents only once every CTA of its instance arrived at the
+  // instance barrier (so vsum's CTAs can never take the SMs a waiting chunk still needs).
   const bool defer_wait = warp == 0 && lane == 0;
   if (!defer_wait) {
     griddep_wait();
-    griddep_launch_dependents();
+    if (!SPLIT) griddep_launch_dependents();
   }
   if (warp == 0) {
     // ===================== producer: left_k / left_v panels =====================
     if (lane == 0) {
       auto load_p = [&] {  // P operand image (bf16 hi/lo, already swizzled by qdots) -> smem in one bulk copy
         griddep_wait();
-        griddep_launch_dependents();
+        if (!SPLIT) griddep_launch_dependents();
         const uint32_t pbytes = 2u * p.kpk * NP * 128;
         mbar_expect_tx(&bars[kPopReady], pbytes);
         bulk_load(smem + L.phi, reinterpret_cast<const unsigned char*>(a.ws_pimg) + static_cast<size_t>(b) * pbytes,
@@ -531,8 +554,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rel = is_v ? i - it.lv0 : i - it.lk0;
         const int per_tile = is_v ? p.mtiles : p.kst;
         const int tile = rel / per_tile, pair = rel % per_tile;
-        if (a.trace && i == it.lv0) a.trace[blockIdx.x * 16ull + 10] = global_ns();
-        if (a.trace && i == it.total - 1) a.trace[blockIdx.x * 16ull + 14] = global_ns();  // last stage issued
+        if (a.trace && i == it.lv0) a.trace[blockIdx.x * 32ull + 10] = global_ns();
+        if (a.trace && i == it.total - 1) a.trace[blockIdx.x * 32ull + 14] = global_ns();  // last stage issued
         // packed panel-major layout: the panels (2 pair, 2 pair + 1) of a tile are contiguous;
         // a missing odd V panel stays unloaded (U rows >= rank_v are never read)
         const long gtile = static_cast<long>(a.inst0 + b) * p.ntiles + it.tile0 + tile;
@@ -556,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t pt2 = smem_addr(smem + L.pt2);
       mbar_wait(&bars[kPopReady], 0);
       tc_fence_after();
-      if (a.trace) a.trace[blockIdx.x * 16ull + 8] = global_ns();
+      if (a.trace) a.trace[blockIdx.x * 32ull + 8] = global_ns();
       for (int t = 0; t < it.tiles; ++t) {
         for (int pp = 0; pp < p.kst; ++pp) {
           const int i = it.lk0 + t * p.kst + pp, s = i % NS;
@@ -573,12 +596,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       mma_commit(&bars[kSFull]);
-      if (a.trace) a.trace[blockIdx.x * 16ull + 9] = global_ns();
+      if (a.trace) a.trace[blockIdx.x * 32ull + 9] = global_ns();
       for (int t = 0; t < it.tiles; ++t) {
         const int buf = t & 1;
         mbar_wait(&bars[kPFull0 + buf], (t >> 1) & 1);
         tc_fence_after();
-        if (a.trace && t < 3) a.trace[blockIdx.x * 16ull + 11 + t] = global_ns();  // p tile t seen by the MMA
+        if (a.trace && t < 3) a.trace[blockIdx.x * 32ull + 11 + t] = global_ns();  // p tile t seen by the MMA
         const uint32_t pth = pt + buf * 4 * NP * 128;
         const uint32_t pth2 = pt2 + buf * 4 * NP * 128;
         for (int mt = 0; mt < p.mtiles; ++mt) {
@@ -599,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(&bars[kPEmpty0 + buf]);
       }
-      if (a.trace) a.trace[blockIdx.x * 16ull + 7] = global_ns();  // last U MMA issued
+      if (a.trace) a.trace[blockIdx.x * 32ull + 7] = global_ns();  // last U MMA issued
       mma_commit(&bars[kUFull]);
       mbar_wait(&bars[kTmemFree], 0);
     }
@@ -620,7 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* f_me = stats + 3 * NP;  // exp(m_loc - m_g) / z_g   (my tokens' softmax correction)
     float* zi_g = stats + 4 * NP;  // 1 / z_g
     float* scale_c = stats + 5 * NP;  // [C][NP]: exp(m_c - m_g) per peer
-    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 0] = global_ns();
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 32ull + 0] = global_ns();
 
     // prefetch my importance scores and tail logits (latency off the critical path)
     const float* tg = a.ws_tail + static_cast<long>(b) * H * p.s.tail_cap;
@@ -642,7 +665,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto tmem_row = [&](uint32_t col) { return tmem + (static_cast<uint32_t>(qd * 32) << 16) + col; };
     mbar_wait(&bars[kSFull], 0);
     tc_fence_after();
-    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 1] = global_ns();
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 32ull + 1] = global_ns();
     float* part_m = part;                         // [16 warps][NP]
     float* part_s = part + kComputeWarps * NP;    // [16 warps][NP]
     for (int c0 = 0; c0 < gcols; c0 += 4) {
@@ -667,7 +690,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       m_loc[h] = m;
     }
     named_bar(kBarCompute, kComputeThreads);
-    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 2] = global_ns();
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 32ull + 2] = global_ns();
 
     // ---- p tiles with the local max (bf16 hi/lo B operand, K-major over tokens); z from the same pass
     float zp[gcols];
@@ -724,9 +747,51 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < it.n_tk; ++j) z += stail[j * NP + h];
       z_loc[h] = z;
     }
-    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 3] = global_ns();
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 32ull + 3] = global_ns();
 
     // ---- publish (m_loc, z_loc); global statistics while the U MMAs still run
+    if constexpr (SPLIT) {
+      float* st_me = a.ws_stats + (static_cast<long>(b) * C + c) * 2 * H;
+      if (tid < H) {
+        st_me[tid] = m_loc[tid];
+        st_me[H + tid] = z_loc[tid];
+      }
+      named_bar(kBarCompute, kComputeThreads);
+      if (tid == 0) {
+        // release: the stats the compute warps wrote before the barrier above are visible to any
+        // CTA that acquires the counter (the CUTLASS generic-barrier pattern, no full fence)
+        if (a.trace) a.trace[blockIdx.x * 32ull + 16] = global_ns();
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&a.ws_count[b]) : "memory");
+        if (a.trace) a.trace[blockIdx.x * 32ull + 17] = global_ns();
+        unsigned seen;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(&a.ws_count[b]) : "memory");
+          if (seen < static_cast<unsigned>(C)) __nanosleep(32);
+        } while (seen < static_cast<unsigned>(C));
+        if (a.trace) a.trace[blockIdx.x * 32ull + 18] = global_ns();
+        griddep_launch_dependents();
+      }
+      named_bar(kBarCompute, kComputeThreads);
+      // every peer's (m, z) in one round of independent loads -> shared memory (the part buffer is free)
+      float* peer_st = part;
+      const float* st0 = a.ws_stats + static_cast<long>(b) * C * 2 * H;
+      for (int i = tid; i < C * 2 * H; i += kComputeThreads) peer_st[i] = __ldcg(&st0[i]);
+      named_bar(kBarCompute, kComputeThreads);
+      if (tid < H) {
+        const int h = tid;
+        float mg = -INFINITY;
+        for (int peer = 0; peer < C; ++peer) mg = fmaxf(mg, peer_st[peer * 2 * H + h]);
+        float zg = 0.f;
+        for (int peer = 0; peer < C; ++peer) {
+          const float mp = peer_st[peer * 2 * H + h];
+          if (mp != -INFINITY) zg += peer_st[peer * 2 * H + H + h] * __expf(mp - mg);
+        }
+        const float zi = 1.0f / zg;
+        m_g[h] = mg;
+        zi_g[h] = zi;
+        f_me[h] = (m_loc[h] == -INFINITY ? 0.f : __expf(m_loc[h] - mg)) * zi;
+      }
+    } else {
     if (tid == 0) fence_acq_rel_cluster();
     named_bar(kBarCompute, kComputeThreads);
     if (tid < C) mbar_arrive_cluster(&bars[kStats], static_cast<uint32_t>(tid));
@@ -757,8 +822,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       zi_g[h] = zi;
       f_me[h] = (m_loc[h] == -INFINITY ? 0.f : __expf(m_loc[h] - mg)) * zi;
     }
+    }
     named_bar(kBarCompute, kComputeThreads);
-    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 6] = global_ns();  // cluster statistics in hand
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 32ull + 6] = global_ns();  // cluster statistics in hand
 
     // ---- head-averaged attention + importance EMA (importance.cpp:33-65); S re-read
     //      from TMEM concurrently with the U MMAs (disjoint TMEM columns)
@@ -809,66 +875,92 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 
     // ---- U readback (TMEM -> U_loc[h][r]); publish U_loc to the cluster
-    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 15] = global_ns();  // EMA + tail work done
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 32ull + 15] = global_ns();  // EMA + tail work done
     mbar_wait(&bars[kUFull], 0);
     tc_fence_after();
-    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 4] = global_ns();
-    float* uloc = reinterpret_cast<float*>(smem + L.uloc);
-    for (int mt = 0; mt < p.mtiles; ++mt) {
-      const int r = mt * 128 + qd * 32 + lane;
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 32ull + 4] = global_ns();
+    if constexpr (SPLIT) {
+      // this chunk's U, scaled by its softmax correction exp(m_c - m_g) / z_g, as a partial for vsum
+      float* up = a.ws_u + (static_cast<long>(b) * C + c) * H * p.s.rank_v;
+      for (int mt = 0; mt < p.mtiles; ++mt) {
+        const int r = mt * 128 + qd * 32 + lane;
 #pragma unroll
-      for (int c0 = 0; c0 < gcols; c0 += 4) {
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (it.tiles > 0) tld4_hilo<ST>(tmem_row(s_cols + static_cast<uint32_t>(mt * NPW + gbase + c0)), NP, v);
-        if (it.tiles > 0 && mt < p.nb2) {  // second tier contributes to the value-rank prefix only
-          float v2[4];
-          tld4_hilo<ST>(tmem_row(s_cols + static_cast<uint32_t>((p.mtiles + mt) * NPW + gbase + c0)), NP, v2);
-          if (r < p.s.rv2)
-            for (int e = 0; e < 4; ++e) v[e] += v2[e];
-        }
-        for (int e = 0; e < 4; ++e) {
-          const int h = gbase + c0 + e;
-          if (h < H && r < p.s.rank_v) uloc[h * L.uloc_stride + r] = v[e];
+        for (int c0 = 0; c0 < gcols; c0 += 4) {
+          float v[4] = {0.f, 0.f, 0.f, 0.f};
+          if (it.tiles > 0) tld4_hilo<ST>(tmem_row(s_cols + static_cast<uint32_t>(mt * NPW + gbase + c0)), NP, v);
+          if (it.tiles > 0 && mt < p.nb2) {
+            float v2[4];
+            tld4_hilo<ST>(tmem_row(s_cols + static_cast<uint32_t>((p.mtiles + mt) * NPW + gbase + c0)), NP, v2);
+            if (r < p.s.rv2)
+              for (int e = 0; e < 4; ++e) v[e] += v2[e];
+          }
+          for (int e = 0; e < 4; ++e) {
+            const int h = gbase + c0 + e;
+            if (h < H && r < p.s.rank_v) up[static_cast<long>(h) * p.s.rank_v + r] = v[e] * f_me[h];
+          }
         }
       }
-    }
-    tc_fence_before();
-    if (tid == 0) fence_acq_rel_cluster();
-    named_bar(kBarCompute, kComputeThreads);
-    if (tid == 0) mbar_arrive(&bars[kTmemFree]);
-    if (tid < C) mbar_arrive_cluster(&bars[kUReady], static_cast<uint32_t>(tid));
-    mbar_wait_cluster(&bars[kUReady], 0);
+      tc_fence_before();
+      named_bar(kBarCompute, kComputeThreads);
+      if (tid == 0) mbar_arrive(&bars[kTmemFree]);
+    } else {
+      float* uloc = reinterpret_cast<float*>(smem + L.uloc);
+      for (int mt = 0; mt < p.mtiles; ++mt) {
+        const int r = mt * 128 + qd * 32 + lane;
+#pragma unroll
+        for (int c0 = 0; c0 < gcols; c0 += 4) {
+          float v[4] = {0.f, 0.f, 0.f, 0.f};
+          if (it.tiles > 0) tld4_hilo<ST>(tmem_row(s_cols + static_cast<uint32_t>(mt * NPW + gbase + c0)), NP, v);
+          if (it.tiles > 0 && mt < p.nb2) {  // second tier contributes to the value-rank prefix only
+            float v2[4];
+            tld4_hilo<ST>(tmem_row(s_cols + static_cast<uint32_t>((p.mtiles + mt) * NPW + gbase + c0)), NP, v2);
+            if (r < p.s.rv2)
+              for (int e = 0; e < 4; ++e) v[e] += v2[e];
+          }
+          for (int e = 0; e < 4; ++e) {
+            const int h = gbase + c0 + e;
+            if (h < H && r < p.s.rank_v) uloc[h * L.uloc_stride + r] = v[e];
+          }
+        }
+      }
+      tc_fence_before();
+      if (tid == 0) fence_acq_rel_cluster();
+      named_bar(kBarCompute, kComputeThreads);
+      if (tid == 0) mbar_arrive(&bars[kTmemFree]);
+      if (tid < C) mbar_arrive_cluster(&bars[kUReady], static_cast<uint32_t>(tid));
+      mbar_wait_cluster(&bars[kUReady], 0);
 
-    // ---- reduce-scatter U over the cluster: heads h = c, c + C, ...; U / z -> workspace
-    const int r4 = L.uloc_stride / 4;
-    const int my_heads = (H - c + C - 1) / C;
-    for (int w = tid; w < my_heads * r4; w += kComputeThreads) {
-      const int h = c + (w / r4) * C, r = (w % r4) * 4;
-      uint4 u[8];
+      // ---- reduce-scatter U over the cluster: heads h = c, c + C, ...; U / z -> workspace
+      const int r4 = L.uloc_stride / 4;
+      const int my_heads = (H - c + C - 1) / C;
+      for (int w = tid; w < my_heads * r4; w += kComputeThreads) {
+        const int h = c + (w / r4) * C, r = (w % r4) * 4;
+        uint4 u[8];
 #pragma unroll
-      for (int peer = 0; peer < 8; ++peer)
-        if (peer < C) u[peer] = ld_dsmem_v4(&uloc[h * L.uloc_stride + r], static_cast<uint32_t>(peer));
-      float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int peer = 0; peer < 8; ++peer)
+          if (peer < C) u[peer] = ld_dsmem_v4(&uloc[h * L.uloc_stride + r], static_cast<uint32_t>(peer));
+        float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-      for (int peer = 0; peer < 8; ++peer) {
-        if (peer >= C) break;
-        const float sc = scale_c[peer * NP + h];
-        s4.x = fmaf(sc, __uint_as_float(u[peer].x), s4.x);
-        s4.y = fmaf(sc, __uint_as_float(u[peer].y), s4.y);
-        s4.z = fmaf(sc, __uint_as_float(u[peer].z), s4.z);
-        s4.w = fmaf(sc, __uint_as_float(u[peer].w), s4.w);
+        for (int peer = 0; peer < 8; ++peer) {
+          if (peer >= C) break;
+          const float sc = scale_c[peer * NP + h];
+          s4.x = fmaf(sc, __uint_as_float(u[peer].x), s4.x);
+          s4.y = fmaf(sc, __uint_as_float(u[peer].y), s4.y);
+          s4.z = fmaf(sc, __uint_as_float(u[peer].z), s4.z);
+          s4.w = fmaf(sc, __uint_as_float(u[peer].w), s4.w);
+        }
+        const float zi = zi_g[h];
+        float* dst = a.ws_u + (static_cast<long>(b) * H + h) * p.s.rank_v + r;
+        const float vals[4] = {s4.x * zi, s4.y * zi, s4.z * zi, s4.w * zi};
+        for (int e = 0; e < 4; ++e)
+          if (r + e < p.s.rank_v) dst[e] = vals[e];
       }
-      const float zi = zi_g[h];
-      float* dst = a.ws_u + (static_cast<long>(b) * H + h) * p.s.rank_v + r;
-      const float vals[4] = {s4.x * zi, s4.y * zi, s4.z * zi, s4.w * zi};
-      for (int e = 0; e < 4; ++e)
-        if (r + e < p.s.rank_v) dst[e] = vals[e];
+      if (tid == 0) fence_acq_rel_cluster();
+      named_bar(kBarCompute, kComputeThreads);
+      if (tid < C) mbar_arrive_cluster(&bars[kDone], static_cast<uint32_t>(tid));
+      mbar_wait_cluster(&bars[kDone], 0);  // peers may still be reading my U_loc / stats
     }
-    if (tid == 0) fence_acq_rel_cluster();
-    named_bar(kBarCompute, kComputeThreads);
-    if (tid < C) mbar_arrive_cluster(&bars[kDone], static_cast<uint32_t>(tid));
-    mbar_wait_cluster(&bars[kDone], 0);  // peers may still be reading my U_loc / stats
-    if (a.trace && tid == 0) a.trace[blockIdx.x * 16ull + 5] = global_ns();
+    if (a.trace && tid == 0) a.trace[blockIdx.x * 32ull + 5] = global_ns();
   }
 }
 
@@ -888,7 +980,8 @@ FusedPlan plan_fused(const FusedShape& s) {
   if (s.D != 128 && s.D != 64) return bad("fused path needs head_dim 64 or 128");
   if (s.H > 64) return bad("fused path supports up to 64 query heads");
   if (s.rank_k < 1 || s.rank_v < 1) return bad("fused path needs low-rank K and V");
-  if (s.cluster < 1 || s.cluster > 8) return bad("cluster size must be 1..8");
+  p.split = s.split == 1;
+  if (s.cluster < 1 || (!p.split && s.cluster > 8)) return bad("cluster size must be 1..8");
   p.np = (s.H + 15) / 16 * 16;
   p.kpk = (s.rank_k + 63) / 64;
   p.vpanels = ((s.rank_v + 63) / 64 + 1) / 2 * 2;
@@ -932,10 +1025,34 @@ FusedPlan plan_fused(const FusedShape& s) {
   return p;
 }
 
-size_t fused_workspace_bytes(const FusedShape& s) {
-  const size_t np = (s.H + 15) / 16 * 16, kpk = (s.rank_k + 63) / 64;
-  const size_t pimg = 2 * kpk * np * 128;
-  return static_cast<size_t>(s.batch) * (pimg + sizeof(float) * s.H * (static_cast<size_t>(s.tail_cap) + s.rank_v));
+namespace {
+struct WsLayout {
+  size_t pimg, tail, u, stats, count, total;
+};
+WsLayout ws_layout(const FusedShape& s) {
+  const size_t np = (s.H + 15) / 16 * 16, kpk = (s.rank_k + 63) / 64, B = s.batch;
+  const size_t parts = s.split == 1 ? static_cast<size_t>(s.cluster) : 1;
+  WsLayout w{};
+  w.pimg = 0;
+  w.tail = w.pimg + B * 2 * kpk * np * 128;
+  w.u = w.tail + sizeof(float) * B * s.H * s.tail_cap;
+  w.stats = w.u + sizeof(float) * B * parts * s.H * s.rank_v;
+  w.count = w.stats + (s.split == 1 ? sizeof(float) * B * parts * 2 * s.H : 0);
+  w.total = w.count + (s.split == 1 ? sizeof(unsigned) * B : 0);
+  return w;
+}
+}  // namespace
+
+size_t fused_workspace_bytes(const FusedShape& s) { return ws_layout(s).total; }
+
+void bind_workspace(const FusedPlan& p, FusedArgs& a, void* ws) {
+  const WsLayout w = ws_layout(p.s);
+  unsigned char* base = static_cast<unsigned char*>(ws);
+  a.ws_pimg = base + w.pimg;
+  a.ws_tail = reinterpret_cast<float*>(base + w.tail);
+  a.ws_u = reinterpret_cast<float*>(base + w.u);
+  a.ws_stats = p.split ? reinterpret_cast<float*>(base + w.stats) : nullptr;
+  a.ws_count = p.split ? reinterpret_cast<unsigned*>(base + w.count) : nullptr;
 }
 
 // Programmatic dependent launch of the three decode kernels (each waits with
@@ -995,14 +1112,16 @@ void launch_stream(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, bool
 }
 
 using CoreFn = void (*)(const FusedPlan, const FusedArgs);
-CoreFn core_for(int np, bool stack) {
+template <bool SPLIT>
+CoreFn core_for_mode(int np, bool stack) {
   switch (np) {
-    case 16: return stack ? core_kernel<16, true> : core_kernel<16, false>;
-    case 32: return stack ? core_kernel<32, true> : core_kernel<32, false>;
-    case 48: return core_kernel<48, false>;
-    default: return core_kernel<64, false>;
+    case 16: return stack ? core_kernel<16, true, SPLIT> : core_kernel<16, false, SPLIT>;
+    case 32: return stack ? core_kernel<32, true, SPLIT> : core_kernel<32, false, SPLIT>;
+    case 48: return core_kernel<48, false, SPLIT>;
+    default: return core_kernel<64, false, SPLIT>;
   }
 }
+CoreFn core_for(const FusedPlan& p) { return p.split ? core_for_mode<true>(p.np, p.stack) : core_for_mode<false>(p.np, p.stack); }
 
 void launch_qdots(const FusedPlan& p, const FusedArgs& a, cudaStream_t st) { launch_stream(p, a, st, true); }
 void launch_vsum(const FusedPlan& p, const FusedArgs& a, cudaStream_t st) { launch_stream(p, a, st, false); }
@@ -1010,7 +1129,7 @@ void launch_vsum(const FusedPlan& p, const FusedArgs& a, cudaStream_t st) { laun
 int max_active_clusters(const FusedPlan& p);
 
 void launch_core(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, int priority) {
-  auto kernel = core_for(p.np, p.stack);
+  auto kernel = core_for(p);
   KVP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_bytes)));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(p.s.batch * p.s.cluster));
@@ -1018,11 +1137,14 @@ void launch_core(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, int pr
   cfg.dynamicSmemBytes = p.smem_bytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[3];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = static_cast<unsigned>(p.s.cluster);
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  int na = 1;
+  int na = 0;
+  if (!p.split) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(p.s.cluster);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    na = 1;
+  }
   if (priority != 0) {
     attr[na].id = cudaLaunchAttributePriority;
     attr[na++].val.priority = priority;
@@ -1072,7 +1194,7 @@ int max_active_clusters(const FusedPlan& p) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  auto kernel = core_for(p.np, p.stack);
+  auto kernel = core_for(p);
   KVP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(p.smem_bytes)));
   int n = 0;
   KVP_CUDA(cudaOccupancyMaxActiveClusters(&n, kernel, &cfg));
@@ -1162,13 +1284,38 @@ int auto_cluster(kvp::FusedShape s) {
 }
 }  // namespace
 int kvp::auto_cluster_size(const kvp::FusedShape& s) { return auto_cluster(s); }
+
+// Work split of the core: token chunks over all SMs when every CTA of the batch can be
+// co-resident (the per-instance barrier in global memory needs it), else one cluster per
+// instance.  Split: chunks per instance = SMs / batch (capped by the tile count), rounded so
+// every chunk holds the same number of 128-token tiles.
+kvp::FusedShape kvp::resolve_fused_shape(kvp::FusedShape s) {
+  if (s.split == 1 || (s.split < 0 && s.cluster <= 0)) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int ntiles = (s.n_comp + 127) / 128;
+    int C = s.split == 1 && s.cluster > 0 ? s.cluster : std::min(ntiles, sms / std::max(1, s.batch));
+    if (C >= 1) {
+      const int per = (ntiles + C - 1) / C;
+      C = (ntiles + per - 1) / per;
+      kvp::FusedShape t = s;
+      t.split = 1;
+      t.cluster = C;
+      const kvp::FusedPlan p = kvp::plan_fused(t);
+      if ((p.ok && static_cast<long>(s.batch) * C <= sms) || s.split == 1) return t;
+    }
+  }
+  s.split = 0;
+  if (s.cluster <= 0) s.cluster = auto_cluster(s);
+  return s;
+}
 namespace {
 kvp::FusedShape shape_of(const kvp_fused_desc* d) {
   kvp::FusedShape s{d->heads, d->kv_heads, d->head_dim, d->n_comp, d->rank_k, d->rank_v, 0,
                     d->tail_cap, d->batch, d->cluster};
   s.rv2 = d->tier2_value_rank;
-  if (s.cluster <= 0) s.cluster = auto_cluster(s);
-  return s;
+  s.split = d->cluster > 0 ? 0 : -1;  // an explicit cluster size keeps the cluster path
+  return kvp::resolve_fused_shape(s);
 }
 }  // namespace
 
@@ -1229,9 +1376,7 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     a.head_avg = d->head_avg;
     a.ctx_out = d->context;
     a.ctx_bf16 = d->context_bf16;
-    a.ws_pimg = reinterpret_cast<unsigned char*>(ws);
-    a.ws_tail = reinterpret_cast<float*>(a.ws_pimg + static_cast<size_t>(s.batch) * 2 * p.kpk * p.np * 128);
-    a.ws_u = a.ws_tail + static_cast<size_t>(s.batch) * s.H * s.tail_cap;
+    bind_workspace(p, a, ws);
     a.trace = g_trace;
     launch_fused(p, a, st);
   });

@@ -20,6 +20,9 @@ struct FusedShape {
   int batch;
   int cluster;        // CTAs per instance in the low-rank core kernel
   int rv2 = 0;        // two-tier values: rank prefix of the second tier (0 = untiered)
+  int split = -1;     // core work split: 1 = token chunks over all SMs with a per-instance barrier in global
+                      // memory (`cluster` = chunks per instance), 0 = one thread-block cluster per instance
+                      // (DSMEM exchange), -1 = choose (split when the whole batch is co-resident)
 };
 
 struct FusedArgs {
@@ -48,9 +51,13 @@ struct FusedArgs {
   int ctx_bf16;                  // 1: bf16 output, 0: fp32
   // workspace: P operand image (bf16 hi/lo, swizzled) [batch][2][kpk][NP][64],
   //            s_tail / p_tail fp32 [batch][H][tail_cap], U fp32 [batch][H][rank_v]
+  //            (split mode: U partials [batch][chunks][H][rank_v], then (m, z) [batch][chunks][2][H] and
+  //             one arrival counter per instance)
   unsigned char* ws_pimg;
   float* ws_tail;
   float* ws_u;
+  float* ws_stats;
+  unsigned* ws_count;
   unsigned long long* trace;     // debug: per-CTA phase timestamps [grid][16] (nullable)
 };
 
@@ -73,6 +80,7 @@ struct FusedPlan {
   int stages;          // TMA ring stages (even)
   size_t smem_bytes;
   int tmem_cols;
+  bool split;          // token-chunk split over all SMs (global-memory barrier) instead of clusters
   bool ok;
   const char* why;
 };
@@ -80,6 +88,10 @@ struct FusedPlan {
 FusedPlan plan_fused(const FusedShape& s);
 int auto_cluster_size(const FusedShape& s);  // occupancy-aware CTAs per instance
 size_t fused_workspace_bytes(const FusedShape& s);
+// Resolves split / cluster choices of `s` (auto when cluster <= 0 or split < 0).
+FusedShape resolve_fused_shape(FusedShape s);
+// Carves a workspace of fused_workspace_bytes() into the FusedArgs buffers.
+void bind_workspace(const FusedPlan& p, FusedArgs& a, void* ws);
 size_t packed_left_bytes(int batch, int n, int rank);
 void pack_left(const void* src, long ld, int batch, int n, int rank, void* dst, cudaStream_t st);
 void launch_fused(const FusedPlan& p, const FusedArgs& a, cudaStream_t st);

@@ -279,9 +279,7 @@ FusedArgs fused_args(kvp_engine* e, int l, bool append_kv) {
   a.ctx_out = e->ctx;
   a.ctx_bf16 = 1;
   a.vtier = e->vtier ? e->vtier + static_cast<size_t>(lidx) * e->B * e->n : nullptr;
-  a.ws_pimg = static_cast<unsigned char*>(e->fused_ws);
-  a.ws_tail = reinterpret_cast<float*>(a.ws_pimg + static_cast<size_t>(e->B) * 2 * e->plan.kpk * e->plan.np * 128);
-  a.ws_u = a.ws_tail + static_cast<size_t>(e->B) * e->H * e->cap;
+  bind_workspace(e->plan, a, e->fused_ws);
   a.trace = nullptr;
   return a;
 }
@@ -536,7 +534,8 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
       }
     }
     fs.rv2 = e->rv2;
-    if (fs.cluster <= 0) fs.cluster = auto_cluster_size(fs);
+    fs.split = c->cluster > 0 ? 0 : -1;  // an explicit cluster size keeps the cluster path
+    fs = resolve_fused_shape(fs);
     e->plan = plan_fused(fs);
     require(e->plan.ok, KVP_ERR_PARAMETER, (std::string("engine: ") + e->plan.why).c_str());
     KVP_CUDA(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));

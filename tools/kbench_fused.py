@@ -77,20 +77,22 @@ def main():
         capi.check(fn(C.byref(L["desc"]), stream))
     torch.cuda.synchronize()
     if args.trace:
-        cl = args.cluster or 8  # trace buffer sized for the largest cluster
-        buf = torch.zeros(B * cl * 16, dtype=torch.int64, device=dev)
+        cl = max(args.cluster, 18)  # trace buffer sized for the largest CTA count per instance
+        buf = torch.zeros(B * cl * 32, dtype=torch.int64, device=dev)
         capi.lib().kvp_debug_fused_trace.argtypes = [C.c_void_p]
         capi.lib().kvp_debug_fused_trace(buf.data_ptr())
         capi.check(fn(C.byref(layers[0]["desc"]), stream))
         torch.cuda.synchronize()
         capi.lib().kvp_debug_fused_trace(None)
-        capi.lib().kvp_debug_fused_max_clusters.argtypes = [C.POINTER(FusedDesc)]
-        print("max active clusters:", capi.lib().kvp_debug_fused_max_clusters(C.byref(layers[0]["desc"])))
-        t = buf.view(B * cl, 16)[:, :16].double().cpu()
+        if args.cluster > 0:
+            capi.lib().kvp_debug_fused_max_clusters.argtypes = [C.POINTER(FusedDesc)]
+            print("max active clusters:", capi.lib().kvp_debug_fused_max_clusters(C.byref(layers[0]["desc"])))
+        t = buf.view(B * cl, 32)[:, :19].double().cpu()
         t = t[t[:, 0] > 0]
         t0 = t[:, 0].min()
         names = ["start", "S ready", "local stats", "p tiles", "U ready", "end", "cluster stats", "mma U issued",
-                 "mma P ok", "mma S done", "prod LV0", "mma p0 ok", "mma p1 ok", "mma p2 ok", "prod last", "EMA done"]
+                 "mma P ok", "mma S done", "prod LV0", "mma p0 ok", "mma p1 ok", "mma p2 ok", "prod last", "EMA done",
+                 "bar stats", "bar released", "bar passed"]
         rel = (t - t0) / 1000.0
         print("phase (us since first CTA start): median / max over CTAs")
         for k, n_ in enumerate(names):
