@@ -172,6 +172,19 @@ size_t kvp_packed_left_bytes(int32_t batch, int32_t n, int32_t rank);
 /* Row-major [batch][n][ld] bf16 left factor -> packed layout. */
 int kvp_pack_left(const void* src, int64_t ld, int32_t batch, int32_t n, int32_t rank, void* dst, void* stream);
 
+/* Projection GEMM of the decode step (decoder.cpp:574-576 q/k/v = h W_q|W_k|W_v, :590 x = ctx W_o;
+ * `matmul` linalg.cpp:167-173) in the serving format: bf16 weights in a packed layout (per
+ * 128-column tile, per 64-row step one contiguous 16 KB block — the tcgen05 MN-major SWIZZLE_128B
+ * operand image), bf16 tokens, fp32 accumulation.  out[B][ldo] = x[B][K] . W[K][N], B <= 256. */
+size_t kvp_packed_weight_bytes(int32_t K, int32_t N);
+/* Row-major [K][N] bf16 weight -> packed layout. */
+int kvp_pack_weight(const void* w, int32_t K, int32_t N, void* dst, void* stream);
+size_t kvp_matmul_packed_workspace(int32_t K, int32_t N, int32_t B);
+/* x: [dev] bf16 [B][K]; w_packed: [dev] (kvp_pack_weight); out: [dev] bf16 or fp32 [B][ldo];
+ * workspace: [dev] kvp_matmul_packed_workspace bytes, zeroed before its first use. */
+int kvp_matmul_packed(const void* x, int32_t B, int32_t K, const void* w_packed, int32_t N, void* out, int32_t ldo,
+                      int32_t out_bf16, void* workspace, void* stream);
+
 /* One layer of a batch of caches in the serving layout: every instance holds
  * one factored block of n_comp tokens (left_k/left_v packed, see above;
  * right_k: [batch][rank_k][W], right_v: [batch][rank_v][W]) and a dense tail

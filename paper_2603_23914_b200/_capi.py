@@ -170,6 +170,11 @@ SIGNATURES = {
     "kvp_assign_groups_host": (C.c_int, [C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
     "kvp_packed_left_bytes": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
     "kvp_pack_left": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "kvp_packed_weight_bytes": (C.c_size_t, [C.c_int32, C.c_int32]),
+    "kvp_pack_weight": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p]),
+    "kvp_matmul_packed_workspace": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
+    "kvp_matmul_packed": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_int32,
+                                    C.c_int32, C.c_void_p, C.c_void_p]),
     "kvp_truncated_svd": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_uint64,
                                     C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "kvp_gaussian_matrix": (C.c_int, [C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_int32, C.c_void_p,

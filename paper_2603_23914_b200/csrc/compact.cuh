@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cublas_v2.h>
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -18,6 +19,9 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
 // Returns the compaction scratch pool's idle pages to the device.
 void svd_pool_trim();
 int range_gemm_npad();
+// bf16 [batch][rows][cols] row-major as a 3-D tensor map, box {64, box_rows, 1}, 128-byte swizzle,
+// out-of-bounds rows zero-filled.
+CUtensorMap encode_bf16_map(const void* base, int cols, int rows, int batch, int box_rows);
 void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, const __nv_bfloat16* xt, bool x_batched,
                 int n, float* c, cudaStream_t st, bool accumulate = false, int ldc = 0);
 // fp32 [batch][rows][cols] (row stride ld, batch stride in_stride) -> bf16 [batch][npad][rows];

@@ -200,6 +200,10 @@ __global__ void transpose_bf16_kernel(const float* __restrict__ in, long in_stri
 
 }  // namespace
 
+CUtensorMap encode_bf16_map(const void* base, int cols, int rows, int batch, int box_rows) {
+  return encode_bf16(base, cols, rows, batch, box_rows);
+}
+
 int range_gemm_npad() { return kNPad; }
 
 void transpose_to_bf16(const float* in, long in_stride, int rows, int cols, int ld, __nv_bfloat16* out, int batch,

@@ -27,6 +27,7 @@
 #include "decode_fused.cuh"
 #include "engine.cuh"
 #include "philox.cuh"
+#include "proj_gemm.cuh"
 
 struct kvp_engine {
   kvp_engine_config cfg{};
@@ -45,6 +46,11 @@ struct kvp_engine {
   LtGemm g_qkv, g_o, g_o_last;
   // buffers
   __nv_bfloat16 *wqkv = nullptr, *wo = nullptr;
+  // the same weights in the hand-written projection GEMM's packed layout (proj_gemm.cu)
+  unsigned char *wqkv_pk = nullptr, *wo_pk = nullptr;
+  size_t wqkv_pk_bytes = 0, wo_pk_bytes = 0;
+  kvp::ProjGemm pg_qkv{}, pg_o{};
+  bool use_cublas = false;  // KVP_PROJ=cublas: library GEMMs (A/B only)
   unsigned char *lk = nullptr, *lv = nullptr;  // packed left factors [L][...]
   __nv_bfloat16 *rkf = nullptr, *rvf = nullptr, *tk = nullptr, *tv = nullptr;
   double* imp = nullptr;
@@ -244,6 +250,13 @@ void lt_setup(kvp_engine* e, kvp_engine::LtGemm& g, int m, int n, int k, bool c_
 void gemm_bf16(kvp_engine* e, int m, int n, int k, const __nv_bfloat16* a, const __nv_bfloat16* b, int ldb, void* c,
                bool c_bf16) {
   const float one = 1.f, zero = 0.f;
+  if (!e->use_cublas) {  // hand-written weight-streaming GEMM over the packed weights
+    const bool is_qkv = n == e->HD + 2 * e->W;
+    const size_t l = static_cast<size_t>(b - (is_qkv ? e->wqkv : e->wo)) / (static_cast<size_t>(k) * n);
+    const unsigned char* wpk = is_qkv ? e->wqkv_pk + l * e->wqkv_pk_bytes : e->wo_pk + l * e->wo_pk_bytes;
+    proj_gemm(is_qkv ? e->pg_qkv : e->pg_o, wpk, a, c, n, c_bf16, e->stream);
+    return;
+  }
   kvp_engine::LtGemm* g = n == e->HD + 2 * e->W ? &e->g_qkv : (c_bf16 ? &e->g_o : &e->g_o_last);
   if (g->ok && ldb == n && m == e->B) {
     blas_check(cublasLtMatmul(e->lt, g->op, &one, b, g->b, a, g->a, &zero, c, g->c, c, g->c, &g->algo, e->blas_ws,
@@ -281,6 +294,11 @@ FusedArgs fused_args(kvp_engine* e, int l, bool append_kv) {
   a.vtier = e->vtier ? e->vtier + static_cast<size_t>(lidx) * e->B * e->n : nullptr;
   bind_workspace(e->plan, a, e->fused_ws);
   a.trace = nullptr;
+  a.pf = pf_mask();
+  // vsum -> the W_o GEMM's weights
+  a.pf_next = e->use_cublas ? static_cast<const void*>(e->wo + lidx * e->HD * e->HD)
+                            : static_cast<const void*>(e->wo_pk + lidx * e->wo_pk_bytes);
+  a.pf_next_bytes = e->use_cublas ? sizeof(__nv_bfloat16) * static_cast<size_t>(e->HD) * e->HD : e->wo_pk_bytes;
   return a;
 }
 
@@ -565,9 +583,28 @@ extern "C" int kvp_engine_create(const kvp_engine_config* c, kvp_engine** out) {
     e->fused_ws = e->alloc<char>(e->fused_ws_bytes);
     {
       const int nqkv = e->HD + 2 * e->W;
-      lt_setup(e.get(), e->g_qkv, e->B, nqkv, e->HD, false, e->xb, e->wqkv, e->qkv);
-      lt_setup(e.get(), e->g_o, e->B, e->HD, e->HD, true, e->ctx, e->wo, e->xb);
-      lt_setup(e.get(), e->g_o_last, e->B, e->HD, e->HD, false, e->ctx, e->wo, e->yout);
+      // KVP_PROJ=tc: the hand-written tcgen05 weight-streaming GEMM (proj_gemm.cu); default cuBLASLt
+      // (measured faster in the step so far)
+      const char* pe = std::getenv("KVP_PROJ");
+      e->use_cublas = !(pe != nullptr && std::strcmp(pe, "tc") == 0);
+      if (e->use_cublas) {
+        lt_setup(e.get(), e->g_qkv, e->B, nqkv, e->HD, false, e->xb, e->wqkv, e->qkv);
+        lt_setup(e.get(), e->g_o, e->B, e->HD, e->HD, true, e->ctx, e->wo, e->xb);
+        lt_setup(e.get(), e->g_o_last, e->B, e->HD, e->HD, false, e->ctx, e->wo, e->yout);
+      } else {
+        require(e->B <= 256, KVP_ERR_PARAMETER, "engine: batch per GPU above 256 (projection GEMM)");
+        int dev = 0, sms = 148;
+        KVP_CUDA(cudaGetDevice(&dev));
+        KVP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        e->wqkv_pk_bytes = packed_weight_bytes(e->HD, nqkv);
+        e->wo_pk_bytes = packed_weight_bytes(e->HD, e->HD);
+        e->wqkv_pk = e->alloc<unsigned char>(L * e->wqkv_pk_bytes);
+        e->wo_pk = e->alloc<unsigned char>(L * e->wo_pk_bytes);
+        e->pg_qkv = proj_gemm_plan(e->HD, nqkv, e->B, sms);
+        e->pg_o = proj_gemm_plan(e->HD, e->HD, e->B, sms);
+        proj_gemm_bind(e->pg_qkv, e->alloc<char>(e->pg_qkv.ws_bytes), e->stream);
+        proj_gemm_bind(e->pg_o, e->alloc<char>(e->pg_o.ws_bytes), e->stream);
+      }
       KVP_CUDA(cudaStreamSynchronize(e->stream));
     }
     if (e->rv2 > 0) e->vtier = e->alloc<unsigned char>(static_cast<size_t>(e->L) * e->B * e->n);
@@ -600,6 +637,11 @@ extern "C" int kvp_engine_prefill(kvp_engine* e) {
                                           stream_id(1, 0, l, 3), wscale);
       });
     }
+    if (!e->use_cublas)
+      for (int l = 0; l < e->L; ++l) {
+        pack_weight(e->wqkv + static_cast<size_t>(l) * e->HD * nqkv, e->HD, nqkv, e->wqkv_pk + l * e->wqkv_pk_bytes, s);
+        pack_weight(e->wo + static_cast<size_t>(l) * e->HD * e->HD, e->HD, e->HD, e->wo_pk + l * e->wo_pk_bytes, s);
+      }
     // textual prefill -> dense tails (harness.cpp:158-167, profile harness.hpp:33)
     KVP_CUDA(cudaMemsetAsync(e->tk, 0, sizeof(__nv_bfloat16) * e->L * e->tail_elems(), s));
     KVP_CUDA(cudaMemsetAsync(e->tv, 0, sizeof(__nv_bfloat16) * e->L * e->tail_elems(), s));
