@@ -47,7 +47,7 @@ namespace {
 
 using namespace sm100;
 
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 6;
 constexpr uint32_t kStageBytes = 16384;  // one packed 128 x 64 bf16 operand panel
 constexpr uint32_t kRing = 32768;        // ring stage: a panel pair, one 32 KB bulk copy (measured on
                                          // B200: a warp-specialised ring's per-SM stream rate grows with
@@ -73,8 +73,6 @@ constexpr int kStreamMinBlocks = KVP_STREAM_MINB;
 
 struct Smem {
   uint32_t ring, phi, plo, pt, pt2, stail, part, stats, imps, bars, tslot, total;
-  uint32_t wts;  // team: phase-C row weights, after the extra ring slots
-  int xslots;    // team: extra ring slots over the P image / p tiles (live only in the row phases)
   uint32_t uloc;  // late-phase alias over [phi, ...), valid once the U MMAs completed
   int uloc_stride;
 };
@@ -96,21 +94,8 @@ __host__ __device__ inline Smem smem_layout(const FusedPlan& p) {
   const uint32_t pt_end = (s.pt + pt_bytes) > (s.phi + pimg_bytes) ? s.pt + pt_bytes : s.phi + pimg_bytes;
   s.uloc_stride = static_cast<int>(align_up(p.s.rank_v, 4));
   s.uloc = s.phi;
-  uint32_t uloc_end = s.uloc + np * s.uloc_stride * 4;
-  if (p.team) {  // phase-C row weights [NP][rows per CTA] over the same (dead) bytes
-    const uint32_t per_c = static_cast<uint32_t>((p.s.rank_v + p.s.tail_cap + p.s.cluster - 1) / p.s.cluster);
-    if (s.uloc + np * per_c * 4 > uloc_end) uloc_end = s.uloc + np * per_c * 4;
-  }
+  const uint32_t uloc_end = s.uloc + np * s.uloc_stride * 4;
   s.stail = align_up(pt_end > uloc_end ? pt_end : uloc_end, 16);
-  s.xslots = 0;
-  s.wts = s.uloc;
-  if (p.team) {  // [phi, stail) is dead during phases A and C: extra ring slots there, then the C weights
-    const uint32_t per_c = static_cast<uint32_t>((p.s.rank_v + p.s.tail_cap + p.s.cluster - 1) / p.s.cluster);
-    const uint32_t wbytes = align_up(np * per_c * 4, 16);
-    s.xslots = s.stail - s.phi >= wbytes ? static_cast<int>((s.stail - s.phi - wbytes) / kRing) : 0;
-    if (s.xslots + p.stages > kMaxStages) s.xslots = kMaxStages - p.stages;
-    s.wts = s.phi + s.xslots * kRing;
-  }
   s.part = s.stail + p.tail_max * np * 4;
   // part: per-warp softmax partials, then (split) every peer's (m, z), then the EMA's head sums
   const uint32_t part_bytes = 2 * kComputeWarps * np * 4 + 4 * 128 * 4;
@@ -142,23 +127,9 @@ enum Bar : int {
 struct Items {
   int lk0, lv0, total;
   int n_tk, tiles, tile0, chunk_len, c_first, t_first;
-  // team mode: my share of the basis / tail rows of phase A (right_k, tail_k -> P, logits) and phase C
-  // (right_v, tail_v -> output partials), as [rank rows r0, r1) + [tail rows t0, t1); ring stages nA / nC
-  int ar0, ar1, at0, at1, nAr, nA;
-  int cr0, cr1, ct0, ct1, nCr, nC, c0;
-  int ntl;  // tail rows streamed (the appended row is computed from its fp32 source instead)
 };
 
-// [lo, hi) of a contiguous rank-rows-then-tail-rows list of length rk + nt, split evenly over C parts
-__device__ __forceinline__ void row_share(int rk, int nt, int C, int c, int& r0, int& r1, int& t0, int& t1) {
-  const int n = rk + nt, per = (n + C - 1) / C, lo = min(n, c * per), hi = min(n, lo + per);
-  r0 = min(lo, rk);
-  r1 = min(hi, rk);
-  t0 = max(lo, rk) - rk;
-  t1 = max(hi, rk) - rk;
-}
-
-__device__ __forceinline__ Items make_items(const FusedPlan& p, int c, int n_tail, int append) {
+__device__ __forceinline__ Items make_items(const FusedPlan& p, int c, int n_tail) {
   Items it{};
   const int C = p.s.cluster;
   const int tail_per = (n_tail + C - 1) / C;
@@ -168,45 +139,11 @@ __device__ __forceinline__ Items make_items(const FusedPlan& p, int c, int n_tai
   it.tiles = max(0, min(p.ntiles, it.tile0 + p.max_tiles) - it.tile0);
   it.c_first = it.tile0 * 128;
   it.chunk_len = max(0, min(p.s.n_comp - it.c_first, it.tiles * 128));
-  // ring items: [team: phase-A row stages] left_k panel pairs, left_v panel pairs [team: phase-C row stages]
-  it.nA = it.nC = 0;
-  if (p.team) {
-    it.ntl = max(0, n_tail - append);
-    row_share(p.s.rank_k, it.ntl, C, c, it.ar0, it.ar1, it.at0, it.at1);
-    row_share(p.s.rank_v, it.ntl, C, c, it.cr0, it.cr1, it.ct0, it.ct1);
-    it.nAr = (it.ar1 - it.ar0 + p.rps - 1) / p.rps;
-    it.nA = it.nAr + (it.at1 - it.at0 + p.rps - 1) / p.rps;
-    it.nCr = (it.cr1 - it.cr0 + p.rps - 1) / p.rps;
-    it.nC = it.nCr + (it.ct1 - it.ct0 + p.rps - 1) / p.rps;
-  }
-  it.lk0 = it.nA;
-  it.lv0 = it.lk0 + it.tiles * p.kst;        // left_k: panel pairs, one ring stage each
-  it.c0 = it.lv0 + it.tiles * p.mtiles;      // left_v: 128-rank panel pairs
-  it.total = it.c0 + it.nC;
+  // ring items (MMA operands only): left_k panels, even-pad, left_v panels
+  it.lk0 = 0;
+  it.lv0 = it.tiles * p.kst;                 // left_k: panel pairs, one ring stage each
+  it.total = it.lv0 + it.tiles * p.mtiles;   // left_v: 128-rank panel pairs
   return it;
-}
-
-// Ring slot of item i and how many earlier items used that slot (its mbarrier phase).  Core items
-// (left_k, left_v) cycle over the NS ring slots; team row items (phases A and C) also use the
-// nx extra slots laid over the P image / p tiles, which are dead while rows stream.
-__device__ __forceinline__ void slot_of(const Items& it, int NS, int nx, int i, int& slot, int& use) {
-  const int NB = NS + nx, ncore = it.c0 - it.lk0;
-  auto uses_a = [&](int sl) { return it.nA > sl ? (it.nA - 1 - sl) / NB + 1 : 0; };
-  if (i < it.lk0) {
-    slot = i % NB;
-    use = i / NB;
-  } else if (i < it.c0) {
-    const int k = i - it.lk0;
-    slot = k % NS;
-    use = uses_a(slot) + k / NS;
-  } else {
-    const int j = i - it.c0;
-    slot = j % NB;
-    use = uses_a(slot) + (slot < NS && ncore > slot ? (ncore - 1 - slot) / NS + 1 : 0) + j / NB;
-  }
-}
-__device__ __forceinline__ uint32_t slot_off(const Smem& L, int NS, int slot) {
-  return slot < NS ? L.ring + slot * kRing : L.phi + (slot - NS) * kRing;
 }
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -299,6 +236,11 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) qdots_kernel
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / LPH, gl = lane % LPH;
   const int H = p.s.H, W = p.s.Hkv * D;
+  if ((a.pf & 1) && threadIdx.x == 0) {  // core's left_k for instance b -> L2 (independent of q)
+    const long blocks = static_cast<long>(p.ntiles) * p.kpk;
+    const unsigned char* base = a.left_k_packed + static_cast<long>(a.inst0 + b) * blocks * kStageBytes;
+    for (long i = g; i < blocks; i += p.s.Hkv) bulk_prefetch_l2(base + i * kStageBytes, kStageBytes);
+  }
   griddep_wait();               // q (and the new k, v) come from the projection GEMM
   griddep_launch_dependents();  // core may start its q-independent prologue and left_k stream
   if (p.split && g == 0 && threadIdx.x == 0) a.ws_count[b] = 0u;  // core's per-instance barrier (after its wait)
@@ -477,6 +419,13 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) vsum_kernel(
   // triggered this launch) do not depend on core: the first batch is in flight
   // while core finishes.  The weights U / p_tail are core's output.
   issue(r0);
+  if ((a.pf & 16) && a.pf_next && threadIdx.x == 0) {  // the following kernel's operand -> L2
+    const size_t nblk = static_cast<size_t>(gridDim.x) * gridDim.y, me = static_cast<size_t>(b) * gridDim.x + g;
+    const size_t share = (a.pf_next_bytes / nblk + 65535) & ~static_cast<size_t>(65535);
+    const size_t lo = me * share, hi = min(a.pf_next_bytes & ~static_cast<size_t>(15), lo + share);
+    for (size_t o = lo; o < hi; o += 65536)
+      bulk_prefetch_l2(static_cast<const unsigned char*>(a.pf_next) + o, static_cast<uint32_t>(hi - o < 65536 ? hi - o : 65536));
+  }
   griddep_wait();
   if (p.split) {  // U = sum of the token chunks' partials (each already scaled by its softmax correction)
     const int C = p.s.cluster;
@@ -545,21 +494,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) vsum_kernel(
 // softmax statistics through global memory behind a per-instance arrival counter, and write U partials
 // (scaled by their correction factor) for vsum to sum; otherwise one thread-block cluster per instance
 // exchanges through DSMEM and reduce-scatters U.
-// Team barrier in global memory (split mode): arrive with release, wait with acquire until the
-// instance's counter reached `target` (k-th barrier of the launch: k * chunks).
-__device__ __forceinline__ void team_arrive(unsigned* cnt) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
-}
-__device__ __forceinline__ void team_wait(const unsigned* cnt, unsigned target) {
-  unsigned seen;
-  for (;;) {
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(cnt) : "memory");
-    if (seen >= target) break;
-    __nanosleep(32);
-  }
-}
-
-template <int NPT, bool ST, bool SPLIT, bool TEAM>  // ST: hi/lo stacked along N (plan.stack)
+template <int NPT, bool ST, bool SPLIT>  // ST: hi/lo stacked along N (plan.stack)
 __global__ void __launch_bounds__(kThreads, 1)
     core_kernel(const FusedPlan p, const FusedArgs a) {
   constexpr int NPW = ST ? 2 * NPT : NPT;      // TMEM columns of one S / U tile
@@ -574,13 +509,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int H = p.s.H;
   constexpr int NP = NPT;
   const int n_tail = a.n_tail_dev ? *a.n_tail_dev : a.n_tail;
-  const Items it = make_items(p, c, n_tail, TEAM ? a.append_kv : 0);
+  const Items it = make_items(p, c, n_tail);
   const uint32_t s_cols = static_cast<uint32_t>(p.max_tiles * NPW);
   const int NS = p.stages;
 
   // ---- prologue: zero ring + P operand, barriers, TMEM -------------------------
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.stages + L.xslots; ++s) {
+    for (int s = 0; s < p.stages; ++s) {
       mbar_init(&bars[kFull + s], 1);
       mbar_init(&bars[kEmpty + s], 1);
     }
@@ -609,59 +544,40 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ===================== producer: left_k / left_v panels =====================
     if (lane == 0) {
-      const long Wl = static_cast<long>(p.s.Hkv) * p.s.D;
       auto load_p = [&] {  // P operand image (bf16 hi/lo, already swizzled by qdots) -> smem in one bulk copy
         griddep_wait();
         if (!SPLIT) griddep_launch_dependents();
-        if (TEAM) {  // written by the team's phase A (generic proxy) -> read by the bulk copy (async proxy)
-          team_wait(&a.ws_count[b], static_cast<unsigned>(C));
-          fence_proxy_async_all();
-          if (a.trace) a.trace[blockIdx.x * 32ull + 25] = global_ns();  // producer: P load issued
-        }
         const uint32_t pbytes = 2u * p.kpk * NP * 128;
         mbar_expect_tx(&bars[kPopReady], pbytes);
         bulk_load(smem + L.phi, reinterpret_cast<const unsigned char*>(a.ws_pimg) + static_cast<size_t>(b) * pbytes,
                   pbytes, &bars[kPopReady]);
       };
-      bool p_loaded = false, u_done = false;
+      if (a.pf & 2) {  // my left_v tiles -> L2 while left_k streams (they follow the S phase)
+        const long g0 = static_cast<long>(a.inst0 + b) * p.ntiles + it.tile0;
+        const unsigned char* src = a.left_v_packed + g0 * p.vpanels_st * static_cast<long>(kStageBytes);
+        const long bytes = static_cast<long>(it.tiles) * p.vpanels_st * kStageBytes;
+        for (long o = 0; o < bytes; o += kRing) bulk_prefetch_l2(src + o, static_cast<uint32_t>(bytes - o < kRing ? bytes - o : kRing));
+      }
+      if (a.pf & 12) {  // vsum's value basis / tail rows of this instance, my 1/C share -> L2
+        const long W = static_cast<long>(p.s.Hkv) * p.s.D;
+        auto share = [&](const __nv_bfloat16* base, long bytes) {
+          const long per = ((bytes + C - 1) / C + 15) & ~15L, lo = c * per, hi = min(bytes, lo + per) & ~15L;
+          for (long o = lo; o < hi; o += 65536)
+            bulk_prefetch_l2(reinterpret_cast<const unsigned char*>(base) + o, static_cast<uint32_t>(hi - o < 65536 ? hi - o : 65536));
+        };
+        if (a.pf & 4) share(a.right_v + static_cast<long>(b) * p.s.rank_v * W, 2L * p.s.rank_v * W);
+        if (a.pf & 8) share(a.tail_v + static_cast<long>(b) * p.s.tail_cap * W, 2L * n_tail * W);
+      }
+      bool p_loaded = false;
       for (int i = 0; i < it.total; ++i) {
-        if (!p_loaded && i == NS + it.lk0) {  // the ring is full: the MMAs that free it next need P
+        if (i == NS) {  // the ring is full: the MMAs that free it need P
           load_p();
           p_loaded = true;
         }
-        int s, use;
-        slot_of(it, NS, L.xslots, i, s, use);
-        if (TEAM && s >= NS && i >= it.c0 && !u_done) {  // extra slots again: the P image / p tiles are dead
-          mbar_wait(&bars[kUFull], 0);
-          u_done = true;
-        }
-        mbar_wait(&bars[kEmpty + s], (use & 1) ^ 1);
-        unsigned char* dst = smem + slot_off(L, NS, s);
+        const int s = i % NS;
+        mbar_wait(&bars[kEmpty + s], ((i / NS) & 1) ^ 1);
+        unsigned char* dst = smem + L.ring + s * kRing;
         uint64_t* full = &bars[kFull + s];
-        if (TEAM && (i < it.lk0 || i >= it.c0)) {
-          // basis / tail rows of phase A (right_k, tail_k) or phase C (right_v, tail_v): contiguous rows
-          const bool pa = i < it.lk0;
-          const int j = pa ? i : i - it.c0, nr_rank = pa ? it.nAr : it.nCr;
-          const int rk = pa ? p.s.rank_k : p.s.rank_v;
-          const int r0 = pa ? it.ar0 : it.cr0, r1 = pa ? it.ar1 : it.cr1, t0 = pa ? it.at0 : it.ct0,
-                    t1 = pa ? it.at1 : it.ct1;
-          const __nv_bfloat16* src;
-          int rows;
-          if (j < nr_rank) {
-            const int row = r0 + j * p.rps;
-            rows = min(p.rps, r1 - row);
-            src = (pa ? a.right_k : a.right_v) + (static_cast<long>(b) * rk + row) * Wl;
-          } else {
-            const int row = t0 + (j - nr_rank) * p.rps;
-            rows = min(p.rps, t1 - row);
-            src = (pa ? a.tail_k : a.tail_v) + (static_cast<long>(b) * p.s.tail_cap + row) * Wl;
-          }
-          const uint32_t bytes = static_cast<uint32_t>(rows * Wl * 2);
-          if (a.trace && (i == NS || i == NS + 1)) a.trace[blockIdx.x * 32ull + 30 + (i - NS)] = global_ns();
-          mbar_expect_tx(full, bytes);
-          bulk_load(dst, src, bytes, full);
-          continue;
-        }
         const bool is_v = i >= it.lv0;
         const int rel = is_v ? i - it.lv0 : i - it.lk0;
         const int per_tile = is_v ? p.mtiles : p.kst;
@@ -694,10 +610,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (a.trace) a.trace[blockIdx.x * 32ull + 8] = global_ns();
       for (int t = 0; t < it.tiles; ++t) {
         for (int pp = 0; pp < p.kst; ++pp) {
-          const int i = it.lk0 + t * p.kst + pp;
-          int s, use;
-          slot_of(it, NS, L.xslots, i, s, use);
-          mbar_wait(&bars[kFull + s], use & 1);
+          const int i = it.lk0 + t * p.kst + pp, s = i % NS;
+          mbar_wait(&bars[kFull + s], (i / NS) & 1);
           tc_fence_after();
           for (int q = 0; q < 2 && 2 * pp + q < p.kpk; ++q) {
             const int kp = 2 * pp + q;
@@ -719,10 +633,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t pth = pt + buf * 4 * NP * 128;
         const uint32_t pth2 = pt2 + buf * 4 * NP * 128;
         for (int mt = 0; mt < p.mtiles; ++mt) {
-          const int i0 = it.lv0 + t * p.mtiles + mt;
-          int s0, use0;
-          slot_of(it, NS, L.xslots, i0, s0, use0);
-          mbar_wait(&bars[kFull + s0], use0 & 1);
+          const int i0 = it.lv0 + t * p.mtiles + mt, s0 = i0 % NS;
+          mbar_wait(&bars[kFull + s0], (i0 / NS) & 1);
           tc_fence_after();
           const uint32_t d = tmem + s_cols + static_cast<uint32_t>(mt * NPW);
           for (int ks = 0; ks < 8; ++ks)
@@ -760,132 +672,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* zi_g = stats + 4 * NP;  // 1 / z_g
     float* scale_c = stats + 5 * NP;  // [C][NP]: exp(m_c - m_g) per peer
     if (a.trace && tid == 0) a.trace[blockIdx.x * 32ull + 0] = global_ns();
-    const int D = p.s.D, PKV = H / p.s.Hkv;
-    const long Wl = static_cast<long>(p.s.Hkv) * D;
-    const long cap = p.s.tail_cap;
-
-    if constexpr (TEAM) {
-      // ---- phase A (qdots folded in): P[h, r] = right_k[r, g(h)] . q_h / sqrt(D) for my rank rows and the
-      //      tail logits of my tail rows, from the ring; warp cw owns heads cw, cw + 16, ... (q in registers)
-      const float scale = rsqrtf(static_cast<float>(D));
-      // 4 lanes per (row, head) dot, D/4 elements each: thread tid -> head hh, quarter qtr, row slot rs
-      // (rows per pass rpp = 128 / H).  The 16-byte chunks are visited in a per-thread rotated order
-      // (conflict-free LDS.128) and the q registers are stored in that order (static indexing).
-      const int qtr = tid & 3, dslot = tid >> 2, rpp = 128 / H;
-      const int hh = dslot % H, rs = dslot / H, ept = D / 4, nchk = ept / 8;
-      const bool act = rs < rpp;
-      const int rot = nchk == 4 ? ((qtr >> 1) + 2 * (hh & 1)) & 3 : ((qtr >> 1) + (hh & 1)) & 1;
-      float qf[32];
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int ck = (k + rot) & (nchk - 1);
-          qf[k * 8 + e] = (act && k < nchk)
-                              ? a.q[static_cast<long>(b) * a.q_stride + hh * D + qtr * ept + ck * 8 + e] * scale
-                              : 0.f;
-        }
-      const uint32_t plane = static_cast<uint32_t>(p.kpk) * NP * 128;
-      unsigned char* pimg = a.ws_pimg + static_cast<size_t>(b) * 2 * plane;
-      float* tout = a.ws_tail + static_cast<long>(b) * H * cap;
-      const long seg0 = (static_cast<long>(hh / PKV) * D + qtr * ept) * 2;
-      for (int j = 0; j < it.nA; ++j) {
-        int sl, use;
-        slot_of(it, NS, L.xslots, j, sl, use);
-        mbar_wait(&bars[kFull + sl], use & 1);
-        const unsigned char* rb = smem + slot_off(L, NS, sl);
-        const bool rank = j < it.nAr;
-        const int row0 = rank ? it.ar0 + j * p.rps : it.at0 + (j - it.nAr) * p.rps;
-        const int nr = (p.dbg & 1) ? 0 : min(p.rps, (rank ? it.ar1 : it.at1) - row0);
-        if (a.trace && tid == 0 && j < 2) a.trace[blockIdx.x * 32ull + 26 + 2 * j] = global_ns();
-        for (int rb0 = 0; rb0 < nr; rb0 += rpp) {  // warp-uniform trip count
-          const int rr = rb0 + rs;
-          const bool v = act && rr < nr;
-          float d = 0.f;
-          if (v) {
-            const unsigned char* seg = rb + rr * Wl * 2 + seg0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (k >= nchk) break;
-              float x[8];
-              unpack8(*reinterpret_cast<const uint4*>(seg + ((k + rot) & (nchk - 1)) * 16), x);
-#pragma unroll
-              for (int e = 0; e < 8; ++e) d = fmaf(x[e], qf[k * 8 + e], d);
-            }
-          }
-          d += __shfl_xor_sync(0xffffffffu, d, 1);
-          d += __shfl_xor_sync(0xffffffffu, d, 2);
-          if (v && qtr == 0) {
-            if (rank) {
-              const int r = row0 + rr;
-              __nv_bfloat16 hi, lo;
-              split_bf16(d, hi, lo);
-              *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(ST, NP, p.kpk, r >> 6, hh, r & 63, false)) = hi;
-              *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(ST, NP, p.kpk, r >> 6, hh, r & 63, true)) = lo;
-            } else {
-              tout[hh * cap + row0 + rr] = d;
-            }
-          }
-        }
-        if (a.trace && tid == 0 && j < 2) a.trace[blockIdx.x * 32ull + 27 + 2 * j] = global_ns();
-        named_bar(kBarCompute, kComputeThreads);
-        if (tid == 0) mbar_arrive(&bars[kEmpty + sl]);
-      }
-      if (a.append_kv && c == C - 1) {
-        // the step's new k, v (cache.cpp:147-170) -> tail row n_tail - 1; its logits from the fp32 source
-        // rounded to bf16, exactly the stored row (nobody streams it in this launch)
-        const float* src = a.q + static_cast<long>(b) * a.q_stride + static_cast<long>(H) * D;
-        const long row = static_cast<long>(b) * cap + (n_tail - 1);
-        __nv_bfloat16* tk = const_cast<__nv_bfloat16*>(a.tail_k) + row * Wl;
-        __nv_bfloat16* tv = const_cast<__nv_bfloat16*>(a.tail_v) + row * Wl;
-        for (long i = tid; i < Wl; i += kComputeThreads) {
-          tk[i] = __float2bfloat16_rn(src[i]);
-          tv[i] = __float2bfloat16_rn(src[Wl + i]);
-        }
-        for (int h = cw; h < H; h += kComputeWarps) {
-          const float* qh = a.q + static_cast<long>(b) * a.q_stride + h * D;
-          const float* kg = src + (h / PKV) * D;
-          float d = 0.f;
-          for (int e = lane; e < D; e += 32) d = fmaf(__bfloat162float(__float2bfloat16_rn(kg[e])), qh[e] * scale, d);
-          d = warp_sum(d);
-          if (lane == 0) tout[h * cap + n_tail - 1] = d;
-        }
-      }
-      if (c == 0) {  // zero padding of the P image: ranks >= rank_k, heads >= H
-        const int rk = p.s.rank_k, padr = p.kpk * 64 - rk;
-        const __nv_bfloat16 z = __float2bfloat16_rn(0.f);
-        for (int i = tid; i < NP * padr; i += kComputeThreads) {
-          const int h = i / padr, r = rk + i % padr;
-          *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(ST, NP, p.kpk, r >> 6, h, r & 63, false)) = z;
-          *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(ST, NP, p.kpk, r >> 6, h, r & 63, true)) = z;
-        }
-        for (int i = tid; i < (NP - H) * rk; i += kComputeThreads) {
-          const int h = H + i / rk, r = i % rk;
-          *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(ST, NP, p.kpk, r >> 6, h, r & 63, false)) = z;
-          *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(ST, NP, p.kpk, r >> 6, h, r & 63, true)) = z;
-        }
-      }
-      // team barrier 1: every P share and tail logit of the instance written
-      if (a.trace && tid == 0) a.trace[blockIdx.x * 32ull + 19] = global_ns();  // phase A done
-      __threadfence();
-      named_bar(kBarCompute, kComputeThreads);
-      if (tid == 0) {
-        fence_proxy_async_all();
-        team_arrive(&a.ws_count[b]);
-        team_wait(&a.ws_count[b], static_cast<unsigned>(C));
-        if (a.trace) a.trace[blockIdx.x * 32ull + 20] = global_ns();  // barrier 1 passed
-      }
-      named_bar(kBarCompute, kComputeThreads);
-    }
 
     // prefetch my importance scores and tail logits (latency off the critical path)
     const float* tg = a.ws_tail + static_cast<long>(b) * H * p.s.tail_cap;
     if (a.importance) {
       const double* ib = a.importance + static_cast<long>(b) * a.imp_stride;
       for (int i = tid; i < it.chunk_len; i += kComputeThreads) imps[i] = ib[it.c_first + i];
-      for (int j = tid; j < it.n_tk; j += kComputeThreads)  // team: the appended token's score is zeroed here
-        imps[p.chunk + j] = (TEAM && a.append_kv && it.t_first + j == n_tail - 1) ? 0.0
-                                                                                   : ib[p.s.n_comp + it.t_first + j];
+      for (int j = tid; j < it.n_tk; j += kComputeThreads) imps[p.chunk + j] = ib[p.s.n_comp + it.t_first + j];
     }
     for (int i = tid; i < it.n_tk * H; i += kComputeThreads) {
       const int j = i % it.n_tk, h = i / it.n_tk;
@@ -998,9 +791,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (a.trace) a.trace[blockIdx.x * 32ull + 16] = global_ns();
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&a.ws_count[b]) : "memory");
         if (a.trace) a.trace[blockIdx.x * 32ull + 17] = global_ns();
-        team_wait(&a.ws_count[b], static_cast<unsigned>(TEAM ? 2 * C : C));
+        unsigned seen;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(&a.ws_count[b]) : "memory");
+          if (seen < static_cast<unsigned>(C)) __nanosleep(32);
+        } while (seen < static_cast<unsigned>(C));
         if (a.trace) a.trace[blockIdx.x * 32ull + 18] = global_ns();
-        if (!TEAM) griddep_launch_dependents();
+        griddep_launch_dependents();
       }
       named_bar(kBarCompute, kComputeThreads);
       // every peer's (m, z) in one round of independent loads -> shared memory (the part buffer is free)
@@ -1134,104 +931,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       named_bar(kBarCompute, kComputeThreads);
       if (tid == 0) mbar_arrive(&bars[kTmemFree]);
-      if constexpr (TEAM) {
-        // ---- team barrier 3: every U partial and normalised tail weight of the instance written
-        __threadfence();
-        named_bar(kBarCompute, kComputeThreads);
-        if (tid == 0) {
-          team_arrive(&a.ws_count[b]);
-          if (a.trace) a.trace[blockIdx.x * 32ull + 21] = global_ns();  // U partial written
-          team_wait(&a.ws_count[b], static_cast<unsigned>(3 * C));
-          if (a.trace) a.trace[blockIdx.x * 32ull + 22] = global_ns();  // barrier 3 passed
-        }
-        named_bar(kBarCompute, kComputeThreads);
-        // ---- phase C (vsum folded in): weights of my rank rows (U summed over the chunks) and tail rows
-        float* wts = reinterpret_cast<float*>(smem + L.wts);  // behind the extra ring slots
-        const int rv = p.s.rank_v, nrr = it.cr1 - it.cr0, nrow = nrr + (it.ct1 - it.ct0);
-        for (int i = tid; i < H * nrow; i += kComputeThreads) {
-          const int h = i / nrow, j = i % nrow;
-          float w = 0.f;
-          if (j < nrr) {
-            for (int cc = 0; cc < C; ++cc) w += __ldcg(&a.ws_u[((static_cast<long>(b) * C + cc) * H + h) * rv + it.cr0 + j]);
-          } else {
-            w = __ldcg(&a.ws_tail[(static_cast<long>(b) * H + h) * cap + it.ct0 + (j - nrr)]);
-          }
-          wts[h * nrow + j] = w;
-        }
-        named_bar(kBarCompute, kComputeThreads);
-        // thread tid owns the 8-column chunk tid of the W-wide rows (team mode: W <= 4096, one query head
-        // per kv head, so the chunk's head is g = 8 tid / D)
-        float acc[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-        const bool cv = static_cast<long>(tid) * 8 < Wl;
-        const float* wrow = wts + (tid * 8 / D) * nrow;
-        for (int j = 0; j < it.nC; ++j) {
-          int sl, use;
-          slot_of(it, NS, L.xslots, it.c0 + j, sl, use);
-          mbar_wait(&bars[kFull + sl], use & 1);
-          const unsigned char* rb = smem + slot_off(L, NS, sl) + tid * 16;
-          const bool rank = j < it.nCr;
-          const int row0 = rank ? it.cr0 + j * p.rps : it.ct0 + (j - it.nCr) * p.rps;
-          const int nr = (p.dbg & 2) ? 0 : min(p.rps, (rank ? it.cr1 : it.ct1) - row0);
-          const int jb = rank ? row0 - it.cr0 : nrr + row0 - it.ct0;
-          if (cv) {
-            uint4 raw[4];
-#pragma unroll
-            for (int rr = 0; rr < 4; ++rr)  // all loads first (rps <= 4)
-              if (rr < nr) raw[rr] = *reinterpret_cast<const uint4*>(rb + rr * Wl * 2);
-#pragma unroll
-            for (int rr = 0; rr < 4; ++rr) {
-              if (rr >= nr) break;
-              float v[8];
-              unpack8(raw[rr], v);
-              const float w = wrow[jb + rr];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) acc[e] = fmaf(w, v[e], acc[e]);
-            }
-          }
-          named_bar(kBarCompute, kComputeThreads);
-          if (tid == 0) mbar_arrive(&bars[kEmpty + sl]);
-        }
-        const long HD = static_cast<long>(H) * D;
-        float* po = a.ws_out + (static_cast<long>(b) * C + c) * HD;
-        if (cv) {  // head g = 8 tid / D, columns d0.. of its D-slice: output index 8 tid
-          __stcg(reinterpret_cast<float4*>(po + tid * 8), make_float4(acc[0], acc[1], acc[2], acc[3]));
-          __stcg(reinterpret_cast<float4*>(po + tid * 8 + 4), make_float4(acc[4], acc[5], acc[6], acc[7]));
-        }
-        // ---- team barrier 4: every output partial written; my 1/C of the context = their sum
-        __threadfence();
-        named_bar(kBarCompute, kComputeThreads);
-        if (tid == 0) {
-          team_arrive(&a.ws_count[b]);
-          if (a.trace) a.trace[blockIdx.x * 32ull + 23] = global_ns();  // phase C done
-          team_wait(&a.ws_count[b], static_cast<unsigned>(4 * C));
-          if (a.trace) a.trace[blockIdx.x * 32ull + 24] = global_ns();  // barrier 4 passed
-        }
-        named_bar(kBarCompute, kComputeThreads);
-        const long per_o = (HD + C - 1) / C, lo = c * per_o, hi = min(HD, lo + per_o);
-        const float* src_new = a.q + static_cast<long>(b) * a.q_stride + static_cast<long>(H) * D + Wl;
-        for (long e = lo + tid; e < hi; e += kComputeThreads) {
-          float v = 0.f;
-          for (int cc = 0; cc < C; ++cc) v += __ldcg(&a.ws_out[(static_cast<long>(b) * C + cc) * HD + e]);
-          if (a.append_kv) {  // the appended row's value, from its fp32 source rounded to bf16
-            const int h = static_cast<int>(e / D), d = static_cast<int>(e % D);
-            const float pn = __ldcg(&a.ws_tail[(static_cast<long>(b) * H + h) * cap + n_tail - 1]);
-            v = fmaf(pn, __bfloat162float(__float2bfloat16_rn(src_new[(h / PKV) * D + d])), v);
-          }
-          const long oi = static_cast<long>(b) * HD + e;
-          if (a.ctx_bf16) reinterpret_cast<__nv_bfloat16*>(a.ctx_out)[oi] = __float2bfloat16_rn(v);
-          else reinterpret_cast<float*>(a.ctx_out)[oi] = v;
-        }
-        if (tid == 0) {
-          griddep_launch_dependents();
-          // the last CTA to leave resets the instance's counters for the next launch
-          if (atomicAdd(&a.ws_count[p.s.batch + b], 1u) == static_cast<unsigned>(C - 1)) {
-            a.ws_count[b] = 0u;
-            a.ws_count[p.s.batch + b] = 0u;
-          }
-        }
-      }
     } else {
       float* uloc = reinterpret_cast<float*>(smem + L.uloc);
       for (int mt = 0; mt < p.mtiles; ++mt) {
@@ -1310,15 +1009,6 @@ FusedPlan plan_fused(const FusedShape& s) {
   if (s.H > 64) return bad("fused path supports up to 64 query heads");
   if (s.rank_k < 1 || s.rank_v < 1) return bad("fused path needs low-rank K and V");
   p.split = s.split == 1;
-  {  // team mode: split + qdots/vsum folded into the core
-    const char* e = std::getenv("KVP_TEAM");
-    const long W = static_cast<long>(s.Hkv) * s.D;
-    // one query head per kv head and W <= 4096: one 8-column chunk (one head) per compute thread in phase C
-    // measured at C2/C4/C5: no faster than the three launches, so opt-in (KVP_TEAM=1)
-    p.team = p.split && e != nullptr && std::atoi(e) != 0 && s.H == s.Hkv && W <= 8 * kComputeThreads;
-    p.rps = p.team ? static_cast<int>(std::min<long>(4, kRing / (2 * W))) : 0;
-    p.dbg = std::getenv("KVP_TEAM_DBG") ? std::atoi(std::getenv("KVP_TEAM_DBG")) : 0;
-  }
   if (s.cluster < 1 || (!p.split && s.cluster > 8)) return bad("cluster size must be 1..8");
   p.np = (s.H + 15) / 16 * 16;
   p.kpk = (s.rank_k + 63) / 64;
@@ -1365,7 +1055,7 @@ FusedPlan plan_fused(const FusedShape& s) {
 
 namespace {
 struct WsLayout {
-  size_t pimg, tail, u, stats, count, out, total;
+  size_t pimg, tail, u, stats, count, total;
 };
 WsLayout ws_layout(const FusedShape& s) {
   const size_t np = (s.H + 15) / 16 * 16, kpk = (s.rank_k + 63) / 64, B = s.batch;
@@ -1376,9 +1066,7 @@ WsLayout ws_layout(const FusedShape& s) {
   w.u = w.tail + sizeof(float) * B * s.H * s.tail_cap;
   w.stats = w.u + sizeof(float) * B * parts * s.H * s.rank_v;
   w.count = w.stats + (s.split == 1 ? sizeof(float) * B * parts * 2 * s.H : 0);
-  // split: one barrier counter per instance (+ one departure counter in team mode); team: output partials
-  w.out = w.count + (s.split == 1 ? (sizeof(unsigned) * 2 * B + 15) / 16 * 16 : 0);
-  w.total = w.out + (s.split == 1 ? sizeof(float) * B * parts * s.H * s.D : 0);
+  w.total = w.count + (s.split == 1 ? sizeof(unsigned) * B : 0);
   return w;
 }
 }  // namespace
@@ -1393,11 +1081,18 @@ void bind_workspace(const FusedPlan& p, FusedArgs& a, void* ws) {
   a.ws_u = reinterpret_cast<float*>(base + w.u);
   a.ws_stats = p.split ? reinterpret_cast<float*>(base + w.stats) : nullptr;
   a.ws_count = p.split ? reinterpret_cast<unsigned*>(base + w.count) : nullptr;
-  a.ws_out = p.split ? reinterpret_cast<float*>(base + w.out) : nullptr;
 }
 
 // Programmatic dependent launch of the three decode kernels (each waits with
 // griddepcontrol.wait before reading its predecessor's output).  KVP_PDL=0 turns it off.
+int pf_mask() {
+  static const int m = [] {
+    const char* e = std::getenv("KVP_PF");
+    return e == nullptr ? 0 : std::atoi(e);
+  }();
+  return m;
+}
+
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("KVP_PDL");
@@ -1453,27 +1148,19 @@ void launch_stream(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, bool
 }
 
 using CoreFn = void (*)(const FusedPlan, const FusedArgs);
-template <bool SPLIT, bool TEAM>
+template <bool SPLIT>
 CoreFn core_for_mode(int np, bool stack) {
   switch (np) {
-    case 16: return stack ? core_kernel<16, true, SPLIT, TEAM> : core_kernel<16, false, SPLIT, TEAM>;
-    case 32: return stack ? core_kernel<32, true, SPLIT, TEAM> : core_kernel<32, false, SPLIT, TEAM>;
-    case 48: return core_kernel<48, false, SPLIT, TEAM>;
-    default: return core_kernel<64, false, SPLIT, TEAM>;
+    case 16: return stack ? core_kernel<16, true, SPLIT> : core_kernel<16, false, SPLIT>;
+    case 32: return stack ? core_kernel<32, true, SPLIT> : core_kernel<32, false, SPLIT>;
+    case 48: return core_kernel<48, false, SPLIT>;
+    default: return core_kernel<64, false, SPLIT>;
   }
 }
-CoreFn core_for(const FusedPlan& p) {
-  if (p.team) return core_for_mode<true, true>(p.np, p.stack);
-  return p.split ? core_for_mode<true, false>(p.np, p.stack) : core_for_mode<false, false>(p.np, p.stack);
-}
+CoreFn core_for(const FusedPlan& p) { return p.split ? core_for_mode<true>(p.np, p.stack) : core_for_mode<false>(p.np, p.stack); }
 
-// Team mode: the core launch does qdots' and vsum's work.
-void launch_qdots(const FusedPlan& p, const FusedArgs& a, cudaStream_t st) {
-  if (!p.team) launch_stream(p, a, st, true);
-}
-void launch_vsum(const FusedPlan& p, const FusedArgs& a, cudaStream_t st) {
-  if (!p.team) launch_stream(p, a, st, false);
-}
+void launch_qdots(const FusedPlan& p, const FusedArgs& a, cudaStream_t st) { launch_stream(p, a, st, true); }
+void launch_vsum(const FusedPlan& p, const FusedArgs& a, cudaStream_t st) { launch_stream(p, a, st, false); }
 
 int max_active_clusters(const FusedPlan& p);
 
@@ -1527,7 +1214,6 @@ FusedArgs offset_args(const FusedPlan& full, const FusedArgs& a, int b0) {
   o.ws_pimg += static_cast<size_t>(b0) * 2 * full.kpk * full.np * 128;
   o.ws_tail += b0 * H * full.s.tail_cap;
   o.ws_u += b0 * H * full.s.rank_v;
-  // (split / team workspaces are indexed by instance inside the kernels; offset_args serves the cluster path)
   o.inst0 = a.inst0 + b0;
   return o;
 }
@@ -1699,7 +1385,6 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     if (ws == nullptr) {
       own = std::make_unique<Scratch>(ws_bytes, st);
       ws = own->as<float>();
-      KVP_CUDA(cudaMemsetAsync(ws, 0, ws_bytes, st));  // split-mode barrier counters start at zero
     } else {
       require(d->workspace_bytes >= ws_bytes, KVP_ERR_PARAMETER, "decode_fused: workspace too small");
     }
@@ -1729,6 +1414,7 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     a.ctx_bf16 = d->context_bf16;
     bind_workspace(p, a, ws);
     a.trace = g_trace;
+    a.pf = pf_mask();
     launch_fused(p, a, st);
   });
 }

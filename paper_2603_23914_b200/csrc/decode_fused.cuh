@@ -57,9 +57,14 @@ struct FusedArgs {
   float* ws_tail;
   float* ws_u;
   float* ws_stats;
-  unsigned* ws_count;            // split: per-instance barrier counter; team: + departure counter [batch]
-  float* ws_out;                 // team: output partials [batch][chunks][H*D]
+  unsigned* ws_count;
   unsigned long long* trace;     // debug: per-CTA phase timestamps [grid][16] (nullable)
+  // L2 prefetch of the next phase's bytes (cp.async.bulk.prefetch.L2), issued by a phase whose own
+  // stream leaves HBM idle: bit 0 qdots -> core's left_k, bit 1 core -> its own left_v, bit 2 core ->
+  // vsum's right_v, bit 3 core -> vsum's tail_v, bit 4 vsum -> pf_next (the following kernel's operand)
+  int pf;
+  const void* pf_next;
+  size_t pf_next_bytes;
 };
 
 struct FusedPlan {
@@ -82,11 +87,6 @@ struct FusedPlan {
   size_t smem_bytes;
   int tmem_cols;
   bool split;          // token-chunk split over all SMs (global-memory barrier) instead of clusters
-  bool team;           // split mode with qdots and vsum folded into the core (one launch per layer): the
-                       // instance's CTAs also split the rank / tail rows of right_k, tail_k (P, logits) and
-                       // right_v, tail_v (output partials), synchronised by global-memory team barriers
-  int rps;             // team: basis / tail rows per 32 KB ring stage
-  int dbg;             // KVP_TEAM_DBG (timing experiments only)
   bool ok;
   const char* why;
 };
@@ -100,6 +100,7 @@ FusedShape resolve_fused_shape(FusedShape s);
 void bind_workspace(const FusedPlan& p, FusedArgs& a, void* ws);
 size_t packed_left_bytes(int batch, int n, int rank);
 void pack_left(const void* src, long ld, int batch, int n, int rank, void* dst, cudaStream_t st);
+int pf_mask();  // KVP_PF: default L2-prefetch bits of FusedArgs::pf
 void launch_fused(const FusedPlan& p, const FusedArgs& a, cudaStream_t st);
 // The three launches separately (engine pipelining across instance groups).
 void launch_qdots(const FusedPlan& p, const FusedArgs& a, cudaStream_t st);

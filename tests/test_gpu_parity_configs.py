@@ -138,13 +138,6 @@ def test_fused_matches_reference_at_config_shape(name):
         assert np.array_equal(imp[b, n + nt:], case["imp"][b, n + nt:])
 
 
-@pytest.mark.parametrize("name", ["c2", "c4_8x", "c5"])
-def test_fused_team_mode_matches_reference(name, monkeypatch):
-    """Team mode (KVP_TEAM=1): qdots and vsum folded into the split core, one launch per layer."""
-    monkeypatch.setenv("KVP_TEAM", "1")
-    test_fused_matches_reference_at_config_shape(name)
-
-
 # ---------------------------------------------------------------------------
 # Philox Gaussian generator, bit-level, against the reference's own draws
 # ---------------------------------------------------------------------------
