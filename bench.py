@@ -400,10 +400,13 @@ def main():
     att_ms1, att_bytes1 = eng.time_attention(iters=3)
     peak, peak_src = load_peaks()
     achieved = att_bytes1 / (att_ms1 * 1e-3) / 1e9
+    # DRAM bytes per layer from the committed ncu capture, only when it was taken at this run's final tail
     traffic = None
     ncu_file = ROOT / "profiles" / f"ncu_attention_{args.config}.json"
     if ncu_file.exists():
-        traffic = json.loads(ncu_file.read_text()).get("dram_bytes_per_layer")
+        nj = json.loads(ncu_file.read_text())
+        if nj.get("tail_tokens") == cfg["textual"] + steps and nj.get("batch", B) == B:
+            traffic = nj.get("dram_bytes_per_layer")
     # cache path (attention + EMA launches of every layer) at the mean of the run's first and last tail
     cache_ms_step = 0.5 * (att_ms0 + att_ms1) * cfg["layers"]
     cache_path = max_over_ranks(cache_ms_step, world)

@@ -28,4 +28,20 @@ void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, c
 // lo: the bf16 residual x - bf16(x) instead.
 void transpose_to_bf16(const float* in, long in_stride, int rows, int cols, int ld, __nv_bfloat16* out, int batch,
                        cudaStream_t st, bool lo = false);
+// Small dense factorisations of the randomized SVD (small_linalg.cu).
+// g: [batch][k][k] fp64 symmetric (overwritten); lo: [batch][k][k] fp64 lower factor,
+// g + shift_rel*trace/k*I = lo lo^T; lf (optional): fp32 copy with reciprocal diagonal (trsm_rows
+// operand); perm: [batch][k] (identity).
+void chol_batched(double* g, int k, int batch, double shift_rel, double* lo, float* lf, int* perm, cudaStream_t st);
+// q (row-major [batch][n][k]) = y L^-T (columns in step order); q must not alias y.
+void trsm_rows(const float* y, float* q, int n, int k, int batch, const float* lf, const int* perm, cudaStream_t st);
+// The same with fp64 arithmetic against the fp64 factor lo (precise path).
+void trsm_rows_f64(const float* y, float* q, int n, int k, int batch, const double* lo, const int* perm,
+                   cudaStream_t st);
+// Eigenvectors of C = lo lo^T by one-sided block Jacobi on the columns of lo (fp32 work matrix x:
+// [batch][jacobi_kp(k)]^2, flags: [max_sweeps][batch] ints); us/ui: column-major k x R Ritz factors
+// (U_R s_R, U_R / s_R), sv: descending singular values of the top R (optional).
+int jacobi_kp(int k);
+void jacobi_eig(const double* lo, int k, int batch, int R, float* x, int* flags, int max_sweeps, float tol,
+                double rank_tol, float* us, float* ui, float* sv, cudaStream_t st);
 }  // namespace kvp

@@ -377,8 +377,7 @@ __global__ void f32_to_bf16_kernel(const float* in, __nv_bfloat16* out, long n) 
 
 // Visual prefill K/V of every instance of layer l, fp32 [2B][T][W] (K of b at 2b, V at 2b+1),
 // from the latent-factor model with the reference's Philox streams.
-void generate_visual(kvp_engine* e, int l, float* a, float* zbuf, float* lbuf) {
-  cudaStream_t s = e->stream;
+void generate_visual(kvp_engine* e, int l, float* a, float* zbuf, float* lbuf, cudaStream_t s, cublasHandle_t blas) {
   const auto& pr = e->cfg.visual;
   const int T = e->n, W = e->W, D = e->D, Hkv = e->Hkv;
   const int r = pr.true_rank, sh = std::min(pr.shared_subspace, pr.true_rank);
@@ -396,7 +395,7 @@ void generate_visual(kvp_engine* e, int l, float* a, float* zbuf, float* lbuf) {
       });
       // out[:, h*D:(h+1)*D] = z (T x r) * L_h (r x D), batched over heads, ldc = W
       const float one = 1.f, zero = 0.f;
-      blas_check(cublasGemmStridedBatchedEx(e->blas, CUBLAS_OP_N, CUBLAS_OP_N, D, T, r, &one, lbuf, CUDA_R_32F, D,
+      blas_check(cublasGemmStridedBatchedEx(blas, CUBLAS_OP_N, CUBLAS_OP_N, D, T, r, &one, lbuf, CUDA_R_32F, D,
                                             static_cast<long long>(r) * D, zbuf, CUDA_R_32F, r, 0, &zero, out,
                                             CUDA_R_32F, W, D, Hkv, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT),
                  "latent gemm");
@@ -419,62 +418,112 @@ void compact_visual(kvp_engine* e) {
   const int T = e->n, W = e->W;
   const int nb = 2 * e->B;
   const auto& pr = e->cfg.visual;
-  float* a = nullptr;
-  float *zbuf = nullptr, *lbuf = nullptr, *left = nullptr, *right = nullptr;
-  __nv_bfloat16* lb = nullptr;
+  const int R = e->rk;
+  const size_t per_layer = static_cast<size_t>(nb) * T * W;  // fp32 elements of one layer's segments
+  // The synthetic K/V of a chunk of layers is generated first (untimed: in serving they are the
+  // prefill's output, already in HBM), then the chunk is compacted with several layers in flight on
+  // their own streams, so the latency-bound factorisations of one layer (Cholesky, Jacobi rounds)
+  // overlap the others' and the tensor-core range finder.  Chunk = the layers whose inputs fit a
+  // 40 GB staging budget.
+  size_t free_b = 0, total_b = 0;
+  KVP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const size_t budget = std::min<size_t>(40ull << 30, free_b / 4);
+  const int chunk = std::max(1, std::min<int>(e->L, static_cast<int>(budget / (per_layer * sizeof(float)))));
+  // layers in flight: up to 4, as the device memory left after the staging allows (~3x a layer's
+  // fp32 inputs of SVD scratch per lane)
+  constexpr int kMaxLanes = 4;
+  const size_t lane_bytes = 3 * per_layer * sizeof(float);
+  const size_t left_after = free_b > static_cast<size_t>(chunk) * per_layer * sizeof(float)
+                                ? free_b - static_cast<size_t>(chunk) * per_layer * sizeof(float)
+                                : 0;
+  const int kLanes = std::max(1, std::min<int>(kMaxLanes, static_cast<int>(left_after / 2 / lane_bytes)));
+  struct Lane {
+    cudaStream_t s = nullptr;
+    cublasHandle_t blas = nullptr;
+    float *left = nullptr, *right = nullptr;
+    __nv_bfloat16* lb = nullptr;
+  } lanes[kMaxLanes];
   const int rmax = std::max(e->rk, e->rv);
-  KVP_CUDA(cudaMallocAsync(&a, sizeof(float) * nb * T * W, s));
+  for (int i = 0; i < kLanes; ++i) {
+    Lane& ln = lanes[i];
+    if (i == 0) {
+      ln.s = s;
+      ln.blas = e->blas;
+    } else {
+      KVP_CUDA(cudaStreamCreateWithFlags(&ln.s, cudaStreamNonBlocking));
+      blas_check(cublasCreate(&ln.blas), "cublasCreate");
+      blas_check(cublasSetStream(ln.blas, ln.s), "cublasSetStream");
+    }
+    KVP_CUDA(cudaMallocAsync(&ln.left, sizeof(float) * nb * T * rmax, s));
+    KVP_CUDA(cudaMallocAsync(&ln.right, sizeof(float) * nb * rmax * W, s));
+    KVP_CUDA(cudaMallocAsync(&ln.lb, sizeof(__nv_bfloat16) * nb * T * rmax, s));
+  }
+  float *a = nullptr, *zbuf = nullptr, *lbuf = nullptr;
+  KVP_CUDA(cudaMallocAsync(&a, sizeof(float) * per_layer * chunk, s));
   KVP_CUDA(cudaMallocAsync(&zbuf, sizeof(float) * T * pr.true_rank, s));
   KVP_CUDA(cudaMallocAsync(&lbuf, sizeof(float) * e->Hkv * pr.true_rank * e->D, s));
-  KVP_CUDA(cudaMallocAsync(&left, sizeof(float) * nb * T * rmax, s));
-  KVP_CUDA(cudaMallocAsync(&right, sizeof(float) * nb * rmax * W, s));
-  KVP_CUDA(cudaMallocAsync(&lb, sizeof(__nv_bfloat16) * nb * T * rmax, s));
-  const int R = e->rk;
-  // compaction time = the SVD + packing only (the synthetic K/V generation is excluded)
-  std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(e->L));
+  const int nchunks = (e->L + chunk - 1) / chunk;
+  std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(nchunks) + 1);
   for (auto& x : ev) KVP_CUDA(cudaEventCreate(&x));
-  for (int l = 0; l < e->L; ++l) {
-    generate_visual(e, l, a, zbuf, lbuf);
-    KVP_CUDA(cudaEventRecord(ev[2 * l], s));
-    // SvdOptions.method (linalg.hpp:12-19): exact = full sketch with fp32 products (as kvp_truncated_svd)
-    const bool exact = e->cfg.svd_method == 0;
-    randomized_svd_batched(e->blas, s, a, nb, T, W, R, e->cfg.svd_seed,
-                           exact ? std::min(T, W) : e->cfg.svd_oversampling,
-                           exact ? 2 : e->cfg.svd_power_iterations, left, right, exact);
-    // split K (even) / V (odd) matrices into the layer's buffers
-    for (int kind = 0; kind < 2; ++kind) {
-      for (int b = 0; b < e->B; ++b) {
-        const size_t m = static_cast<size_t>(b) * 2 + kind;
-        __nv_bfloat16* rdst = (kind == 0 ? e->rkf + static_cast<size_t>(l) * e->right_k_elems()
-                                         : e->rvf + static_cast<size_t>(l) * e->right_v_elems()) +
-                              static_cast<size_t>(b) * R * W;
-        const long nr = static_cast<long>(R) * W;
-        launch_1d(nr, [&](unsigned g, int t) { f32_to_bf16_kernel<<<g, t, 0, s>>>(right + m * R * W, rdst, nr); });
-        const long nlft = static_cast<long>(T) * R;
-        launch_1d(nlft, [&](unsigned g, int t) {
-          f32_to_bf16_kernel<<<g, t, 0, s>>>(left + m * T * R, lb + static_cast<size_t>(b) * T * R, nlft);
-        });
+  for (int c = 0; c < nchunks; ++c) {
+    const int l0 = c * chunk, l1 = std::min(e->L, l0 + chunk);
+    for (int l = l0; l < l1; ++l) generate_visual(e, l, a + (l - l0) * per_layer, zbuf, lbuf, s, e->blas);
+    KVP_CUDA(cudaEventRecord(ev[2 * c], s));
+    for (int i = 1; i < kLanes; ++i) KVP_CUDA(cudaStreamWaitEvent(lanes[i].s, ev[2 * c], 0));
+    for (int l = l0; l < l1; ++l) {
+      Lane& ln = lanes[(l - l0) % kLanes];
+      cudaStream_t ls = ln.s;
+      // SvdOptions.method (linalg.hpp:12-19): exact = full sketch with fp32 products (as kvp_truncated_svd)
+      const bool exact = e->cfg.svd_method == 0;
+      randomized_svd_batched(ln.blas, ls, a + (l - l0) * per_layer, nb, T, W, R, e->cfg.svd_seed,
+                             exact ? std::min(T, W) : e->cfg.svd_oversampling,
+                             exact ? 2 : e->cfg.svd_power_iterations, ln.left, ln.right, exact);
+      // split K (even) / V (odd) matrices into the layer's buffers
+      for (int kind = 0; kind < 2; ++kind) {
+        for (int b = 0; b < e->B; ++b) {
+          const size_t m = static_cast<size_t>(b) * 2 + kind;
+          __nv_bfloat16* rdst = (kind == 0 ? e->rkf + static_cast<size_t>(l) * e->right_k_elems()
+                                           : e->rvf + static_cast<size_t>(l) * e->right_v_elems()) +
+                                static_cast<size_t>(b) * R * W;
+          const long nr = static_cast<long>(R) * W;
+          launch_1d(nr, [&](unsigned g, int t) { f32_to_bf16_kernel<<<g, t, 0, ls>>>(ln.right + m * R * W, rdst, nr); });
+          const long nlft = static_cast<long>(T) * R;
+          launch_1d(nlft, [&](unsigned g, int t) {
+            f32_to_bf16_kernel<<<g, t, 0, ls>>>(ln.left + m * T * R, ln.lb + static_cast<size_t>(b) * T * R, nlft);
+          });
+        }
+        unsigned char* dst = kind == 0 ? e->lk + static_cast<size_t>(l) * e->lk_bytes()
+                                       : e->lv + static_cast<size_t>(l) * e->lv_bytes();
+        pack_left(ln.lb, R, e->B, T, R, dst, ls);
       }
-      unsigned char* dst = kind == 0 ? e->lk + static_cast<size_t>(l) * e->lk_bytes()
-                                     : e->lv + static_cast<size_t>(l) * e->lv_bytes();
-      pack_left(lb, R, e->B, T, R, dst, s);
     }
-    KVP_CUDA(cudaEventRecord(ev[2 * l + 1], s));
+    // join the lanes back into the engine stream (the next chunk's generation reuses `a`)
+    for (int i = 1; i < kLanes; ++i) {
+      KVP_CUDA(cudaEventRecord(ev[2 * nchunks], lanes[i].s));
+      KVP_CUDA(cudaStreamWaitEvent(s, ev[2 * nchunks], 0));
+    }
+    KVP_CUDA(cudaEventRecord(ev[2 * c + 1], s));
   }
   KVP_CUDA(cudaStreamSynchronize(s));
   double svd_ms = 0.0;
-  for (int l = 0; l < e->L; ++l) {
+  for (int c = 0; c < nchunks; ++c) {
     float ms = 0.f;
-    KVP_CUDA(cudaEventElapsedTime(&ms, ev[2 * l], ev[2 * l + 1]));
+    KVP_CUDA(cudaEventElapsedTime(&ms, ev[2 * c], ev[2 * c + 1]));
     svd_ms += ms;
   }
   for (auto& x : ev) cudaEventDestroy(x);
   e->svd_ms = svd_ms;
-  for (void* p : {static_cast<void*>(a), static_cast<void*>(zbuf), static_cast<void*>(lbuf), static_cast<void*>(left),
-                  static_cast<void*>(right), static_cast<void*>(lb)})
-    KVP_CUDA(cudaFreeAsync(p, s));
+  for (void* p : {static_cast<void*>(a), static_cast<void*>(zbuf), static_cast<void*>(lbuf)}) KVP_CUDA(cudaFreeAsync(p, s));
+  for (int i = 0; i < kLanes; ++i) {
+    for (void* p : {static_cast<void*>(lanes[i].left), static_cast<void*>(lanes[i].right), static_cast<void*>(lanes[i].lb)})
+      KVP_CUDA(cudaFreeAsync(p, s));
+  }
   // prefill staging goes back to the device (the pool keeps pages mapped during compaction)
   KVP_CUDA(cudaStreamSynchronize(s));
+  for (int i = 1; i < kLanes; ++i) {
+    cublasDestroy(lanes[i].blas);
+    cudaStreamDestroy(lanes[i].s);
+  }
   int dev = 0;
   cudaMemPool_t pool;
   if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)

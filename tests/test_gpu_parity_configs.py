@@ -183,3 +183,23 @@ def test_compaction_c2_shape_within_1p02_of_reference():
           f"|right right^T - I| {orth:.2e}")
     assert err <= 1.02 * ref_err
     assert orth <= 1e-4
+
+
+def test_compaction_c4_4x_shape_within_1p02_of_reference():
+    # C4 4x (Qwen-VL-shaped 4096 x 4096 segment, rank 512): the sketch (520) spans two 384-column
+    # tensor-core blocks and the 520 x 520 eigenproblem 36 Jacobi blocks
+    _torch()
+    ref = _ref()
+    from paper_2603_23914_b200 import kvpack
+    from oracle import kvpack_oracle as ko
+    T, H, D, R = 4096, 32, 128, 512
+    a = ref.latent_factor_matrix(T, H, H, D, 2 * R, 0.98, R, 1e-2, 11, ko.stream_id(2, 0, 0, 0))
+    left, right = kvpack.truncated_svd(a, R, method="randomized", seed=0)
+    err = np.linalg.norm(a - left @ right) / np.linalg.norm(a)
+    rl, rr = ref.truncated_svd(a, R, method="randomized", seed=0)
+    ref_err = np.linalg.norm(a - rl @ rr) / np.linalg.norm(a)
+    orth = np.abs(right @ right.T - np.eye(R)).max()
+    print(f"C4 4x compaction: rel err {err:.5f} vs reference {ref_err:.5f} (ratio {err / ref_err:.4f}), "
+          f"|right right^T - I| {orth:.2e}")
+    assert err <= 1.02 * ref_err
+    assert orth <= 1e-4

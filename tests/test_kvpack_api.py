@@ -56,6 +56,37 @@ def test_truncated_svd_matches_numpy():  # test_smoke.py:29-39, fp32: 1e-5 relat
 
 
 @pytest.mark.gpu
+def test_truncated_svd_rank_deficient_keeps_orthonormal_rows():
+    # rank 5 < requested 8 (linalg.cpp:26-29: zero singular values keep orthonormal right rows):
+    # the device Jacobi eigensolver leaves the null components dead, the complement fills them
+    _gpu()
+    rng = np.random.default_rng(8)
+    a = rng.standard_normal((40, 5)) @ rng.standard_normal((5, 24))
+    for method in ("exact", "randomized"):
+        left, right = kvpack.truncated_svd(a, 8, method=method, seed=2)
+        assert np.abs(a - left @ right).max() <= 1e-4 * np.abs(a).max()
+        assert np.abs(right @ right.T - np.eye(8)).max() <= 1e-5
+        # rank prefix 5 already reconstructs the matrix
+        assert np.abs(a - left[:, :5] @ right[:5]).max() <= 1e-4 * np.abs(a).max()
+
+
+@pytest.mark.gpu
+def test_singular_values_graded_spectrum():
+    # the one-sided block Jacobi (small_linalg.cu) against LAPACK on a spectrum spanning 1e3 (the
+    # fp32 sketch products and CholeskyQR keep ~1e-3 relative accuracy down to ~1e-3 of the top
+    # singular value)
+    _gpu()
+    rng = np.random.default_rng(9)
+    u, _ = np.linalg.qr(rng.standard_normal((96, 64)))
+    v, _ = np.linalg.qr(rng.standard_normal((80, 64)))
+    s = np.logspace(0, -3, 64)
+    a = (u * s) @ v.T
+    got = kvpack.singular_values(a)
+    assert np.allclose(got[:64], s, rtol=2e-3, atol=1e-6 * s[0])
+    assert np.all(got[64:] <= 1e-5 * s[0])
+
+
+@pytest.mark.gpu
 def test_randomized_svd_close_to_optimal():  # test_smoke.py:42-50
     _gpu()
     rng = np.random.default_rng(4)

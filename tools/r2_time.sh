@@ -1,0 +1,8 @@
+#!/bin/bash
+mkdir -p gpurun_out/r2
+T=$1
+{
+timeout 300 python tools/check_compaction.py 2304 4096 368 1
+timeout 300 python tools/tcompact.py c2 8
+timeout 300 python tools/tcompact.py c2 32
+} > gpurun_out/r2/time_$T.txt 2>&1
