@@ -262,8 +262,8 @@ void apply_linv(SvdWork& w, const float* y, float* q, int m, int k, int batch, c
     const int cw = std::min(npad, k - c0);
     // X^T rows c = columns c0 + c of L^-T, i.e. rows of L^-1
     transpose_to_bf16(linv_t + c0, static_cast<long>(k) * k, k, cw, k, xh, batch, w.stream);
-    transpose_to_bf16(linv_t + c0, static_cast<long>(k) * k, k, cw, k, xl, batch, w.stream, true);
     range_gemm(yh, m, k, batch, false, xh, true, cw, q + c0, w.stream, false, k);
+    transpose_to_bf16(linv_t + c0, static_cast<long>(k) * k, k, cw, k, xl, batch, w.stream, true);
     range_gemm(yh, m, k, batch, false, xl, true, cw, q + c0, w.stream, true, k);
     range_gemm(yl, m, k, batch, false, xh, true, cw, q + c0, w.stream, true, k);
   }
