@@ -315,6 +315,9 @@ int kvp_cache_get_importance(kvp_cache* cache, uint64_t* positions /*table_size,
 /* Shape: table size, next_position, steps_taken; per segment blocks and tail length. */
 int kvp_cache_shape(kvp_cache* cache, int32_t* table_size, uint64_t* next_position, uint64_t* steps_taken,
                     int32_t* n_blocks /*[2]*/, int32_t* tail_len /*[2]*/);
+/* next_position / steps_taken of every instance (LayerCache fields, cache.hpp:137-146), e.g. from a
+ * KVPK snapshot (snapshot.cpp:275-276); next_position may not move below an assigned position. */
+int kvp_cache_set_counters(kvp_cache* cache, uint64_t next_position, uint64_t steps_taken);
 /* One block store of one instance: tokens and stored rank (0 = dense). */
 int kvp_cache_block_info(kvp_cache* cache, int32_t instance, int32_t modality, int32_t block, int32_t kind,
                          int32_t* tokens, int32_t* rank);

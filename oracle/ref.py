@@ -74,6 +74,8 @@ def lib():
         _lib.kvref_cache_new.restype = C.c_void_p
         _lib.kvref_cache_new.argtypes = [C.c_int, C.c_size_t, C.c_size_t, C.c_size_t, C.c_size_t]
         _lib.kvref_cache_free.argtypes = [C.c_void_p]
+        _lib.kvref_save_cache.argtypes = [C.c_void_p, C.c_char_p, C.c_size_t]
+        _lib.kvref_load_cache.argtypes = [C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]
     return _lib
 
 
@@ -112,6 +114,21 @@ class RefCache:
         if getattr(self, "_h", None):
             lib().kvref_cache_free(C.c_void_p(self._h))
             self._h = None
+
+    def save(self, path: str, width: int = 8):
+        """save_cache (snapshot.cpp:251-307)."""
+        _check(lib().kvref_save_cache(C.c_void_p(self._h), path.encode(), width))
+
+    @classmethod
+    def load(cls, path: str, heads, kv_heads, head_dim, dtype="f64"):
+        """load_cache (snapshot.cpp:309-371)."""
+        h = C.c_void_p()
+        _check(lib().kvref_load_cache(1 if dtype == "f32" else 0, path.encode(), C.byref(h)))
+        obj = cls.__new__(cls)
+        obj.H, obj.Hkv, obj.D = heads, kv_heads, head_dim
+        obj.W, obj.HD, obj.dtype = kv_heads * head_dim, heads * head_dim, dtype
+        obj._h = h.value
+        return obj
 
     def append(self, modality: int, k, v):
         k, v = _f64(k), _f64(v)

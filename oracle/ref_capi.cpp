@@ -19,6 +19,7 @@
 #include "kvpack/harness.hpp"
 #include "kvpack/importance.hpp"
 #include "kvpack/linalg.hpp"
+#include "kvpack/snapshot.hpp"
 
 using namespace kvpack;
 
@@ -127,6 +128,20 @@ void* kvref_cache_new(int dtype, std::size_t heads, std::size_t kv_heads, std::s
 }
 
 void kvref_cache_free(void* h) { delete static_cast<AnyCache*>(h); }
+
+// KVPK snapshots through the reference's own save_cache / load_cache (snapshot.cpp:251-371).
+int kvref_save_cache(void* h, const char* path, std::size_t width) {
+    return guarded([&] { with_cache(h, [&](auto& c) { save_cache(c, std::string(path), width); }); });
+}
+
+int kvref_load_cache(int dtype, const char* path, void** out) {
+    return guarded([&] {
+        if (dtype == 1)
+            *out = new AnyCache(std::in_place_type<LayerCache<float>>, load_cache<float>(std::string(path)));
+        else
+            *out = new AnyCache(std::in_place_type<LayerCache<double>>, load_cache<double>(std::string(path)));
+    });
+}
 
 int kvref_append(void* h, int modality, std::size_t n, const double* k, const double* v) {
     return guarded([&] {

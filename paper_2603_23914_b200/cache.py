@@ -216,6 +216,7 @@ class LayerCacheBatch:
 
     def __init__(self, heads, kv_heads, head_dim, batch=1, dtype="f64", layer_index=0):
         self.H, self.Hkv, self.D, self.batch, self.dtype = heads, kv_heads, head_dim, batch, dtype
+        self.layer_index = layer_index
         self.W, self.HD = kv_heads * head_dim, heads * head_dim
         self._h = C.c_void_p()
         cfg = capi.CacheConfigC(heads, kv_heads, head_dim, _DT[dtype], batch, layer_index)

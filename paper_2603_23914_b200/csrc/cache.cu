@@ -1309,6 +1309,19 @@ extern "C" int kvp_cache_shape(kvp_cache* c, int32_t* table_size, uint64_t* next
   });
 }
 
+// Restores LayerCache.next_position / steps_taken from a host image (a KVPK snapshot records
+// both, snapshot.cpp:275-276); positions already assigned must stay below next_position.
+extern "C" int kvp_cache_set_counters(kvp_cache* c, uint64_t next_position, uint64_t steps_taken) {
+  return guarded([&] {
+    checked(c);
+    require(next_position >= c->next_position, KVP_ERR_PARAMETER,
+            "set_counters: next_position below an assigned position");
+    c->next_position = next_position;
+    c->steps_taken = steps_taken;
+  });
+}
+
+
 namespace {
 const kvp::DBlock& block_at(kvp_cache* c, int inst, int modality, int block) {
   require(inst >= 0 && inst < c->cfg.batch, KVP_ERR_PARAMETER, "cache: instance out of range");

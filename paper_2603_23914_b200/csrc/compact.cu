@@ -236,11 +236,16 @@ void gemm_rm(SvdWork& w, bool ta, bool tb, int m, int n, int k, const float* a, 
 // q = y L^-T for row-major y [batch][m][k], L the fp64 factor.  On the tensor cores when the
 // shape allows (tc): L^-T = I L^-T from the triangular solve of the k identity rows, then the product as
 // a three-term bf16 hi/lo GEMM (y_hi L_hi + y_hi L_lo + y_lo L_hi, ~2^-16 relative) in
-// 384-column blocks; otherwise (the precise path) the row-blocked fp64 triangular solve of every row.
+// 384-column blocks; a shape outside the TMA rules (k or m not a multiple of 8) takes the fp32
+// row-blocked triangular solve, the precise path (tc false) the fp64 one.
 void apply_linv(SvdWork& w, const float* y, float* q, int m, int k, int batch, const double* lo, const float* lf,
                 const int* perm, bool tc) {
-  if (!tc || k % 8 != 0 || m % 8 != 0) {
+  if (!tc) {
     trsm_rows_f64(y, q, m, k, batch, lo, perm, w.stream);
+    return;
+  }
+  if (k % 8 != 0 || m % 8 != 0) {
+    trsm_rows(y, q, m, k, batch, lf, perm, w.stream);
     return;
   }
   const long nk = static_cast<long>(batch) * k * k, ny = static_cast<long>(batch) * m * k;
@@ -262,10 +267,8 @@ void apply_linv(SvdWork& w, const float* y, float* q, int m, int k, int batch, c
     const int cw = std::min(npad, k - c0);
     // X^T rows c = columns c0 + c of L^-T, i.e. rows of L^-1
     transpose_to_bf16(linv_t + c0, static_cast<long>(k) * k, k, cw, k, xh, batch, w.stream);
-    range_gemm(yh, m, k, batch, false, xh, true, cw, q + c0, w.stream, false, k);
     transpose_to_bf16(linv_t + c0, static_cast<long>(k) * k, k, cw, k, xl, batch, w.stream, true);
-    range_gemm(yh, m, k, batch, false, xl, true, cw, q + c0, w.stream, true, k);
-    range_gemm(yl, m, k, batch, false, xh, true, cw, q + c0, w.stream, true, k);
+    range_gemm3(yh, yl, m, k, batch, false, xh, xl, true, cw, q + c0, w.stream, false, k);
   }
 }
 
@@ -288,9 +291,7 @@ void gemm_tc3(SvdWork& w, const float* a, int rows, int K, const float* xt, int 
     KVP_LAUNCHED();
     pad_rows_bf16_kernel<<<g, 256, 0, w.stream>>>(xt, static_cast<long>(n) * K, c0, cw, K, npad, xl, 1);
     KVP_LAUNCHED();
-    range_gemm(ah, rows, K, batch, false, xh, true, cw, c + c0, w.stream, false, n);
-    range_gemm(ah, rows, K, batch, false, xl, true, cw, c + c0, w.stream, true, n);
-    range_gemm(al, rows, K, batch, false, xh, true, cw, c + c0, w.stream, true, n);
+    range_gemm3(ah, al, rows, K, batch, false, xh, xl, true, cw, c + c0, w.stream, false, n);
   }
 }
 
@@ -357,7 +358,6 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   SvdWork w;
   w.blas = blas;
   w.stream = stream;
-  const int k = std::min(rank + oversampling, std::min(T, W));
   const long sA = static_cast<long>(T) * W;
   const int npad = range_gemm_npad();
   // the tcgen05 range finder (bf16 operands) unless fp32 products are asked for or the shape is outside it
@@ -365,6 +365,11 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   const bool force_fp32 = std::getenv("KVP_SVD_FP32") != nullptr;
   const int min_passes = std::getenv("KVP_SVD_PASSES") ? std::atoi(std::getenv("KVP_SVD_PASSES")) : 1;
   const bool tc = !precise && !force_fp32 && T % 8 == 0 && W % 8 == 0;
+  // k = min(R + p, min(T, W)) (linalg.cpp:74); on the tensor-core path rounded up to a multiple of 8
+  // (a few more oversampling columns) so every k-wide operand is a legal TMA row (16-byte stride):
+  // C3's 284 + 8 = 292 becomes 296
+  int k = std::min(rank + oversampling, std::min(T, W));
+  if (tc) k = std::min((k + 7) / 8 * 8, std::min(T, W));
   // The range finder only needs the subspace, so its products take bf16 operands.
   // The last power-iteration product and B = Q^T A carry the factor values: they
   // use the hi/lo split (KVP_SVD_SPLIT=0 turns it off, for comparison).
@@ -395,11 +400,11 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
       for (int c0 = 0; c0 < k; c0 += npad) {
         const int cw = std::min(npad, k - c0);
         transpose_to_bf16(x + c0, static_cast<long>(xr) * k, xr, cw, k, xt, x_batched ? batch : 1, stream);
-        range_gemm(ab, T, W, batch, trans, xt, x_batched, cw, c + c0, stream, false, k);
         if (three) {
           transpose_to_bf16(x + c0, static_cast<long>(xr) * k, xr, cw, k, xt_lo, x_batched ? batch : 1, stream, true);
-          range_gemm(ab, T, W, batch, trans, xt_lo, x_batched, cw, c + c0, stream, true, k);
-          range_gemm(ab_lo, T, W, batch, trans, xt, x_batched, cw, c + c0, stream, true, k);
+          range_gemm3(ab, ab_lo, T, W, batch, trans, xt, xt_lo, x_batched, cw, c + c0, stream, false, k);
+        } else {
+          range_gemm(ab, T, W, batch, trans, xt, x_batched, cw, c + c0, stream, false, k);
         }
       }
     } else {
@@ -413,10 +418,10 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   orth(w, y, y_spare, T, k, batch, power_iterations > 0 ? min_passes : 2, tc);
   for (int it = 0; it < power_iterations; ++it) {
     product(true, y, true, z, false);  // Z = A^T Q
-    orth(w, z, z_spare, W, k, batch, min_passes, tc);
-    product(false, z, true, y, split && it + 1 == power_iterations);  // Y = A Z
-    orth(w, y, y_spare, T, k, batch, it + 1 == power_iterations ? 2 : min_passes, tc);
-  }
+      orth(w, z, z_spare, W, k, batch, min_passes, tc);
+      product(false, z, true, y, split && it + 1 == power_iterations);  // Y = A Z
+      orth(w, y, y_spare, T, k, batch, it + 1 == power_iterations ? 2 : min_passes, tc);
+    }
   // B^T = A^T Q (W x k); B = Q^T A is its transpose
   float* bt = w.get<float>(static_cast<size_t>(batch) * k * W);
   product(true, y, true, bt, split);
@@ -444,7 +449,7 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
   // randomized SVD at the C2 shape: 1e-5 gives 1.0142x its reconstruction error (cuSOLVER's
   // eigensolver: 1.014x), a 2e-4 stop after 6 sweeps 1.019x.
   constexpr int kMaxSweeps = 12;
-  int* flags = w.get<int>(static_cast<size_t>(kMaxSweeps) * batch);
+  int* flags = w.get<int>(jacobi_ws_ints(k, batch, kMaxSweeps));
   float* us = w.get<float>(static_cast<size_t>(batch) * k * rank);
   float* ui = w.get<float>(static_cast<size_t>(batch) * k * rank);
   float* svw = sv ? sv : w.get<float>(static_cast<size_t>(batch) * rank);

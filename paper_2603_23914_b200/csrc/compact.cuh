@@ -25,6 +25,10 @@ CUtensorMap encode_bf16_map(const void* base, int cols, int rows, int batch, int
 void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, const __nv_bfloat16* xt, bool x_batched,
                 int n, float* c, cudaStream_t st, bool accumulate = false, int ldc = 0);
 // fp32 [batch][rows][cols] (row stride ld, batch stride in_stride) -> bf16 [batch][npad][rows];
+// The three-term hi/lo product a x + a x_lo + a_lo x in one launch (one GEMM with a 3x K loop).
+void range_gemm3(const __nv_bfloat16* a, const __nv_bfloat16* a_lo, int T, int W, int batch, bool trans_a,
+                 const __nv_bfloat16* xt, const __nv_bfloat16* xt_lo, bool x_batched, int n, float* c, cudaStream_t st,
+                 bool accumulate = false, int ldc = 0);
 // lo: the bf16 residual x - bf16(x) instead.
 void transpose_to_bf16(const float* in, long in_stride, int rows, int cols, int ld, __nv_bfloat16* out, int batch,
                        cudaStream_t st, bool lo = false);
@@ -42,6 +46,7 @@ void trsm_rows_f64(const float* y, float* q, int n, int k, int batch, const doub
 // [batch][jacobi_kp(k)]^2, flags: [max_sweeps][batch] ints); us/ui: column-major k x R Ritz factors
 // (U_R s_R, U_R / s_R), sv: descending singular values of the top R (optional).
 int jacobi_kp(int k);
+size_t jacobi_ws_ints(int k, int batch, int max_sweeps);  // ints of the flags workspace
 void jacobi_eig(const double* lo, int k, int batch, int R, float* x, int* flags, int max_sweeps, float tol,
                 double rank_tol, float* us, float* ui, float* sv, cudaStream_t st);
 }  // namespace kvp

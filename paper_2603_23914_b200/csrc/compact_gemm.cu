@@ -40,10 +40,14 @@ constexpr uint32_t kBBytes = kNPad * 128;   // X^T tile per K step: 384 rows x 1
 constexpr uint32_t kGStage = kABytes + kBBytes;
 constexpr uint32_t kGSmem = kGStages * kGStage + 1024;
 
+// terms = 3: the three-term hi/lo product A_hi X_hi + A_hi X_lo + A_lo X_hi in one launch, as one
+// GEMM with a 3x longer K loop (term t of k-step kt = kt / ksteps picks the operand maps), so the
+// three terms share the ring, the TMEM accumulator and one epilogue.
 template <bool TRANS_A>
 __global__ void __launch_bounds__(kGThreads, 1)
-    range_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_x, int M,
-                      int K, int n, int x_batched, float* __restrict__ c, long c_stride, int ldc, int accumulate) {
+    range_gemm_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_x,
+                      const __grid_constant__ CUtensorMap map_a2, const __grid_constant__ CUtensorMap map_x2, int terms,
+                      int M, int K, int n, int x_batched, float* __restrict__ c, long c_stride, int ldc, int accumulate) {
   extern __shared__ __align__(1024) unsigned char gsmem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsmem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[kGStages], empty[kGStages], done;
@@ -52,6 +56,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
   const int mt = blockIdx.x, b = blockIdx.y;
   const int m0 = mt * 128;
   const int ksteps = (K + 63) / 64;  // a partial last step reads zeros (TMA out-of-bounds fill)
+  const int ktotal = ksteps * terms;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kGStages; ++s) {
       mbar_init(&full[s], 1);
@@ -61,6 +66,10 @@ __global__ void __launch_bounds__(kGThreads, 1)
     fence_mbar_init();
     prefetch_tmap(&map_a);
     prefetch_tmap(&map_x);
+    if (terms > 1) {
+      prefetch_tmap(&map_a2);
+      prefetch_tmap(&map_x2);
+    }
   }
   if (warp == 1) tmem_alloc(&tslot, 512);
   tc_fence_before();
@@ -70,30 +79,33 @@ __global__ void __launch_bounds__(kGThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int ks = 0; ks < ksteps; ++ks) {
-        const int s = ks % kGStages;
-        if (ks >= kGStages) mbar_wait(&empty[s], ((ks / kGStages) - 1) & 1);
+      for (int kt = 0; kt < ktotal; ++kt) {
+        const int s = kt % kGStages;
+        const int term = kt / ksteps, ks = kt - term * ksteps;
+        const CUtensorMap* ma = term == 2 ? &map_a2 : &map_a;
+        const CUtensorMap* mx = term == 1 ? &map_x2 : &map_x;
+        if (kt >= kGStages) mbar_wait(&empty[s], ((kt / kGStages) - 1) & 1);
         unsigned char* sa = smem + s * kGStage;
         unsigned char* sb = sa + kABytes;
         mbar_expect_tx(&full[s], kGStage);
         if (!TRANS_A) {
           // A tile: rows m0..m0+127 (T), columns ks*64.. (W): one K-major SW128 panel
-          tma_load_3d(sa, &map_a, ks * 64, m0, b, &full[s]);
+          tma_load_3d(sa, ma, ks * 64, m0, b, &full[s]);
         } else {
           // A^T tile (MN-major): K rows ks*64.. (T) x M columns m0..m0+127 (W), two 64-column panels
-          tma_load_3d(sa, &map_a, m0, ks * 64, b, &full[s]);
-          tma_load_3d(sa + kABytes / 2, &map_a, m0 + 64, ks * 64, b, &full[s]);
+          tma_load_3d(sa, ma, m0, ks * 64, b, &full[s]);
+          tma_load_3d(sa + kABytes / 2, ma, m0 + 64, ks * 64, b, &full[s]);
         }
         // X^T tile: rows 0..383 (n), columns ks*64.. (K): two 192-row K-major SW128 panels
-        tma_load_3d(sb, &map_x, ks * 64, 0, x_batched ? b : 0, &full[s]);
-        tma_load_3d(sb + kNHalf * 128, &map_x, ks * 64, kNHalf, x_batched ? b : 0, &full[s]);
+        tma_load_3d(sb, mx, ks * 64, 0, x_batched ? b : 0, &full[s]);
+        tma_load_3d(sb + kNHalf * 128, mx, ks * 64, kNHalf, x_batched ? b : 0, &full[s]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(128, kNHalf, TRANS_A, false);
       const uint32_t base = smem_addr(smem);
-      for (int ks = 0; ks < ksteps; ++ks) {
+      for (int ks = 0; ks < ktotal; ++ks) {
         const int s = ks % kGStages;
         mbar_wait(&full[s], (ks / kGStages) & 1);
         tc_fence_after();
@@ -213,8 +225,9 @@ void transpose_to_bf16(const float* in, long in_stride, int rows, int cols, int 
   KVP_LAUNCHED();
 }
 
-void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, const __nv_bfloat16* xt,
-                bool x_batched, int n, float* c, cudaStream_t st, bool accumulate, int ldc) {
+void range_gemm3(const __nv_bfloat16* a, const __nv_bfloat16* a_lo, int T, int W, int batch, bool trans_a,
+                 const __nv_bfloat16* xt, const __nv_bfloat16* xt_lo, bool x_batched, int n, float* c, cudaStream_t st,
+                 bool accumulate, int ldc) {
   if (ldc <= 0) ldc = n;
   require(n <= kNPad, KVP_ERR_PARAMETER, "compaction: sketch width above 384 (rank + oversampling)");
   require(T % 8 == 0 && W % 8 == 0, KVP_ERR_PARAMETER, "compaction GEMM: T and W must be multiples of 8");
@@ -222,6 +235,9 @@ void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, c
   // A: trans_a=false -> box {64 cols (K), 128 rows (M)}; true -> box {64 cols (M), 64 rows (K)}
   const CUtensorMap ma = encode_bf16(a, W, T, batch, trans_a ? 64 : 128);
   const CUtensorMap mx = encode_bf16(xt, K, kNPad, x_batched ? batch : 1, kNHalf);
+  const bool three = a_lo != nullptr && xt_lo != nullptr;
+  const CUtensorMap ma2 = three ? encode_bf16(a_lo, W, T, batch, trans_a ? 64 : 128) : ma;
+  const CUtensorMap mx2 = three ? encode_bf16(xt_lo, K, kNPad, x_batched ? batch : 1, kNHalf) : mx;
   auto kernel = trans_a ? range_gemm_kernel<true> : range_gemm_kernel<false>;
   static bool attr_set[2] = {false, false};
   if (!attr_set[trans_a]) {
@@ -229,9 +245,14 @@ void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, c
     attr_set[trans_a] = true;
   }
   const dim3 grid((M + 127) / 128, batch);
-  kernel<<<grid, kGThreads, kGSmem, st>>>(ma, mx, M, K, n, x_batched ? 1 : 0, c, static_cast<long>(M) * ldc,
-                                          ldc, accumulate ? 1 : 0);
+  kernel<<<grid, kGThreads, kGSmem, st>>>(ma, mx, ma2, mx2, three ? 3 : 1, M, K, n, x_batched ? 1 : 0, c,
+                                          static_cast<long>(M) * ldc, ldc, accumulate ? 1 : 0);
   KVP_LAUNCHED();
+}
+
+void range_gemm(const __nv_bfloat16* a, int T, int W, int batch, bool trans_a, const __nv_bfloat16* xt,
+                bool x_batched, int n, float* c, cudaStream_t st, bool accumulate, int ldc) {
+  range_gemm3(a, nullptr, T, W, batch, trans_a, xt, nullptr, x_batched, n, c, st, accumulate, ldc);
 }
 
 }  // namespace kvp

@@ -5,8 +5,8 @@
 // Reference steps (linalg.cpp:68-105): thin_q = Eigen::HouseholderQR of the
 // sketch (linalg.cpp:80-84) and the BDCSVD of B = Q^T A (linalg.cpp:93).  Here:
 //
-//   thin_q(Y)  -> shifted CholeskyQR:  G = Y^T Y,  G + shift = L L^T  (chol_kernel, fp64,
-//                 one CTA per matrix, blocked right-looking),  Q = Y L^-T
+//   thin_q(Y)  -> shifted CholeskyQR:  G = Y^T Y,  G + shift = L L^T  (fp64, blocked right-looking:
+//                 a panel launch and a tiled trailing-update launch per 32 columns),  Q = Y L^-T
 //                 (trsm_rows_kernel: blocked forward substitution, 32 rows of Y
 //                 per CTA, warp-shuffle triangular core).
 //   SVD of B   -> C = B B^T (k x k, fp64); Cholesky C = X X^T (a round-off sized
@@ -32,133 +32,148 @@
 namespace kvp {
 namespace {
 
-constexpr int kCholThreads = 512;
 
 // ---------------------------------------------------------------------------
-// Batched Cholesky, fp64, one CTA per matrix, blocked right-looking.
-//   s    : [batch][k][k] symmetric input (lower triangle read), overwritten by the
-//          trailing updates
-//   lo   : [batch][k][k] lower factor L (upper part written as zeros), g + shift = L L^T
-//   lf   : optional [batch][k][k] fp32 copy of L with the diagonal replaced by its
-//          reciprocal (the trsm_rows operand)
+// Batched Cholesky, fp64, blocked right-looking over 32-column panels, two launches per panel:
+//   chol_panel_kernel  (one CTA per matrix): factor the 32 x 32 diagonal block in shared memory
+//                      (one warp, lane = row), then the panel below it, L_iJ = S_iJ L_JJ^-T
+//                      (one thread per row, forward substitution in registers);
+//   chol_update_kernel (one CTA per 32 x 32 tile of the trailing lower triangle, every matrix):
+//                      S_im -= L_iJ L_mJ^T.
+//   s    : [batch][k][k] symmetric input (lower triangle read), overwritten by the updates
+//   lo   : [batch][k][k] lower factor L (zeros above), g + shift = L L^T
+//   lf   : optional fp32 copy of L with the diagonal replaced by its reciprocal (trsm_rows operand)
 //   perm : [batch][k] identity (the trsm_rows interface takes a column order)
-// Each panel of nbp columns is staged in shared memory once and factored there
-// (two barriers per column); the trailing update S -= P P^T touches the lower
-// triangle only.  shift = shift_rel * trace/k: the shifted CholeskyQR of the range
-// finder uses 1e-5 / 1e-7, the PSD factorisations a round-off sized 1e-13 (a
-// semidefinite C then factors without pivoting; its null directions get columns of
-// size sqrt(shift), far below the rank tolerance).  A non-positive pivot gives a
-// zero column.
+// shift = shift_rel * trace/k (chol_prep_kernel): the shifted CholeskyQR of the range finder uses
+// 1e-5 / 1e-7, the PSD factorisations a round-off sized 1e-13 (a semidefinite C then factors
+// without pivoting; its null directions get columns of size sqrt(shift), far below the rank
+// tolerance).  A non-positive pivot gives a zero column.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kCholThreads, 1)
-    chol_kernel(double* __restrict__ s_all, int k, int nbp, double shift_rel, double* __restrict__ lo_all,
-                float* __restrict__ lf_all, int* __restrict__ perm_all) {
-  extern __shared__ double csm[];
-  const int lds = nbp + 1;  // panel row stride (odd: no bank conflicts across rows)
-  double* P = csm;          // [k][lds] panel, rows in place (rows < j0 unused)
-  __shared__ double red_v[kCholThreads / 32];
-  __shared__ double s_shift;
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int nwarps = blockDim.x >> 5;
+constexpr int kCp = 32;  // panel width
+
+__global__ void chol_prep_kernel(double* __restrict__ s_all, int k, double shift_rel, int* __restrict__ perm_all) {
+  __shared__ double red[32];
+  const int b = blockIdx.x, tid = threadIdx.x;
   double* S = s_all + static_cast<size_t>(b) * k * k;
-  double* lo = lo_all + static_cast<size_t>(b) * k * k;
-  int* perm = perm_all + static_cast<size_t>(b) * k;
   double tr = 0.0;
   for (int i = tid; i < k; i += blockDim.x) {
     tr += S[static_cast<size_t>(i) * k + i];
-    perm[i] = i;
+    perm_all[static_cast<size_t>(b) * k + i] = i;
   }
   for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(0xffffffffu, tr, o);
-  if (lane == 0) red_v[warp] = tr;
+  if ((tid & 31) == 0) red[tid >> 5] = tr;
   __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    for (int w = 0; w < nwarps; ++w) t += red_v[w];
-    s_shift = shift_rel * t / k + 1e-300;
+  if (tid < 32) {
+    double t = tid < static_cast<int>(blockDim.x >> 5) ? red[tid] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (tid == 0) red[0] = t;
   }
   __syncthreads();
-  const double shift = s_shift;
+  const double shift = shift_rel * red[0] / k + 1e-300;
+  for (int i = tid; i < k; i += blockDim.x) S[static_cast<size_t>(i) * k + i] += shift;
+}
 
-  for (int j0 = 0; j0 < k; j0 += nbp) {
-    const int nb = min(nbp, k - j0);
-    // stage S[j0.., j0..j0+nb) (row-major rows: nb consecutive doubles per row)
-    for (int e = tid; e < (k - j0) * nb; e += blockDim.x) {
-      const int i = j0 + e / nb, t = e % nb;
-      double v = S[static_cast<size_t>(i) * k + j0 + t];
-      if (i == j0 + t) v += shift;
-      P[static_cast<size_t>(i) * lds + t] = v;
-    }
-    __syncthreads();
-    for (int jj = 0; jj < nb; ++jj) {
-      const int j = j0 + jj;
-      // left-looking inside the panel: column jj -= P[:, <jj] P[j, <jj]^T
-      const double* prow = P + static_cast<size_t>(j) * lds;
-      for (int i = j + tid; i < k; i += blockDim.x) {
-        double* irow = P + static_cast<size_t>(i) * lds;
-        double v = irow[jj];
-        for (int t = 0; t < jj; ++t) v = fma(-irow[t], prow[t], v);
-        irow[jj] = v;
-      }
-      __syncthreads();
-      const double piv = prow[jj];
+__global__ void __launch_bounds__(256)
+    chol_panel_kernel(const double* __restrict__ s_all, int k, int j0, double* __restrict__ lo_all) {
+  __shared__ double D[kCp][kCp + 1];
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const double* S = s_all + static_cast<size_t>(b) * k * k;
+  double* lo = lo_all + static_cast<size_t>(b) * k * k;
+  const int nb = min(kCp, k - j0);
+  for (int e = tid; e < kCp * kCp; e += blockDim.x) {
+    const int r = e / kCp, c = e % kCp;
+    D[r][c] = (r < nb && c <= r) ? S[static_cast<size_t>(j0 + r) * k + j0 + c] : 0.0;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    // lane = row r of the diagonal block; column c: pivot, scale, rank-1 update of the rows below
+    for (int c = 0; c < nb; ++c) {
+      const double piv = D[c][c];
       const double l = piv > 0.0 ? sqrt(piv) : 0.0;
       const double inv = piv > 0.0 ? 1.0 / l : 0.0;
-      for (int i = j + 1 + tid; i < k; i += blockDim.x) P[static_cast<size_t>(i) * lds + jj] *= inv;
-      __syncthreads();
-      if (tid == 0) P[static_cast<size_t>(j) * lds + jj] = l;
-      __syncthreads();
+      __syncwarp();
+      if (lane > c && lane < nb) D[lane][c] *= inv;
+      if (lane == c) D[c][c] = l;
+      __syncwarp();
+      if (lane > c && lane < nb) {
+        const double lr = D[lane][c];
+        for (int q = c + 1; q <= lane; ++q) D[lane][q] = fma(-lr, D[q][c], D[lane][q]);
+      }
+      __syncwarp();
     }
-    // panel columns out; zeros above the diagonal
-    for (int e = tid; e < k * nb; e += blockDim.x) {
-      const int i = e / nb, t = e % nb;
-      lo[static_cast<size_t>(i) * k + j0 + t] = (i >= j0 + t) ? P[static_cast<size_t>(i) * lds + t] : 0.0;
-    }
-    // trailing update of the lower triangle: S[i][m] -= sum_t P[i][t] P[m][t], j0+nb <= m <= i
-    const int r0 = j0 + nb, n = k - r0;
-    if (n > 0) {
-      const int tiles = (n + 3) / 4;
-      const int ntri = tiles * (tiles + 1) / 2;
-      for (int tt = tid; tt < ntri; tt += blockDim.x) {
-        // (ta, tb) with tb <= ta from the triangular index
-        int ta = static_cast<int>((sqrt(8.0 * tt + 1.0) - 1.0) * 0.5);
-        while ((ta + 1) * (ta + 2) / 2 <= tt) ++ta;
-        while (ta * (ta + 1) / 2 > tt) --ta;
-        const int tb = tt - ta * (ta + 1) / 2;
-        double acc[4][4] = {};
-        for (int t = 0; t < nb; ++t) {
-          double va[4], vb[4];
-          for (int x = 0; x < 4; ++x) {
-            const int ia = r0 + ta * 4 + x, ib = r0 + tb * 4 + x;
-            va[x] = ia < k ? P[static_cast<size_t>(ia) * lds + t] : 0.0;
-            vb[x] = ib < k ? P[static_cast<size_t>(ib) * lds + t] : 0.0;
-          }
-          for (int x = 0; x < 4; ++x)
-            for (int y = 0; y < 4; ++y) acc[x][y] = fma(va[x], vb[y], acc[x][y]);
-        }
-        for (int x = 0; x < 4; ++x) {
-          const int ia = r0 + ta * 4 + x;
-          if (ia >= k) continue;
-          for (int y = 0; y < 4; ++y) {
-            const int ib = r0 + tb * 4 + y;
-            if (ib > ia) continue;
-            S[static_cast<size_t>(ia) * k + ib] -= acc[x][y];
-          }
-        }
+  }
+  __syncthreads();
+  for (int e = tid; e < nb * nb; e += blockDim.x) {
+    const int r = e / nb, c = e % nb;
+    if (c <= r) lo[static_cast<size_t>(j0 + r) * k + j0 + c] = D[r][c];
+  }
+  // panel below: row i solves x L_JJ^T = S[i][J]
+  for (int i = j0 + nb + tid; i < k; i += blockDim.x) {
+    double x[kCp];
+    const double* srow = S + static_cast<size_t>(i) * k + j0;
+#pragma unroll
+    for (int c = 0; c < kCp; ++c) x[c] = c < nb ? srow[c] : 0.0;
+#pragma unroll
+    for (int c = 0; c < kCp; ++c) {
+      if (c < nb) {
+        double v = x[c];
+        for (int t = 0; t < c; ++t) v = fma(-x[t], D[c][t], v);
+        x[c] = D[c][c] > 0.0 ? v / D[c][c] : 0.0;
       }
     }
-    __syncthreads();
+    double* lrow = lo + static_cast<size_t>(i) * k + j0;
+#pragma unroll
+    for (int c = 0; c < kCp; ++c)
+      if (c < nb) lrow[c] = x[c];
   }
-  if (lf_all) {
-    float* lf = lf_all + static_cast<size_t>(b) * k * k;
-    for (int e = tid; e < k * k; e += blockDim.x) {
-      const int j = e / k, t = e % k;
-      float v = 0.f;
-      const double dd = lo[static_cast<size_t>(j) * k + t];
-      if (t < j) v = static_cast<float>(dd);
-      else if (t == j) v = dd > 0.0 ? static_cast<float>(1.0 / dd) : 0.f;
-      lf[e] = v;
-    }
+}
+
+// Trailing update of the lower triangle below panel j0: one CTA per 32 x 32 tile (ta >= tb).
+__global__ void __launch_bounds__(256)
+    chol_update_kernel(double* __restrict__ s_all, int k, int j0, const double* __restrict__ lo_all) {
+  __shared__ double La[kCp][kCp + 1], Lb[kCp][kCp + 1];
+  const int b = blockIdx.y, tid = threadIdx.x;
+  const int r0 = j0 + kCp;
+  const int tt = blockIdx.x;
+  int ta = static_cast<int>((sqrt(8.0 * tt + 1.0) - 1.0) * 0.5);
+  while ((ta + 1) * (ta + 2) / 2 <= tt) ++ta;
+  while (ta * (ta + 1) / 2 > tt) --ta;
+  const int tb = tt - ta * (ta + 1) / 2;
+  const int i0 = r0 + ta * kCp, m0 = r0 + tb * kCp;
+  double* S = s_all + static_cast<size_t>(b) * k * k;
+  const double* lo = lo_all + static_cast<size_t>(b) * k * k;
+  for (int e = tid; e < kCp * kCp; e += blockDim.x) {
+    const int r = e / kCp, c = e % kCp;
+    La[r][c] = i0 + r < k ? lo[static_cast<size_t>(i0 + r) * k + j0 + c] : 0.0;
+    Lb[r][c] = m0 + r < k ? lo[static_cast<size_t>(m0 + r) * k + j0 + c] : 0.0;
   }
+  __syncthreads();
+  // thread -> row i0 + tid/8, columns m0 + (tid%8)*4 .. +3
+  const int r = tid >> 3, c4 = (tid & 7) * 4;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 8
+  for (int t = 0; t < kCp; ++t) {
+    const double a = La[r][t];
+    for (int x = 0; x < 4; ++x) acc[x] = fma(a, Lb[c4 + x][t], acc[x]);
+  }
+  const int i = i0 + r;
+  if (i >= k) return;
+  for (int x = 0; x < 4; ++x) {
+    const int m = m0 + c4 + x;
+    if (m < k && m <= i) S[static_cast<size_t>(i) * k + m] -= acc[x];
+  }
+}
+
+__global__ void chol_lf_kernel(const double* __restrict__ lo_all, int k, float* __restrict__ lf_all) {
+  const long e = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e >= static_cast<long>(k) * k) return;
+  const size_t off = static_cast<size_t>(blockIdx.y) * k * k;
+  const int j = static_cast<int>(e / k), t = static_cast<int>(e % k);
+  const double dd = lo_all[off + e];
+  float v = 0.f;
+  if (t < j) v = static_cast<float>(dd);
+  else if (t == j) v = dd > 0.0 ? static_cast<float>(1.0 / dd) : 0.f;
+  lf_all[off + e] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -282,7 +297,7 @@ constexpr int kJChunk = 64;    // rows per streamed chunk
 
 __global__ void __launch_bounds__(kJThreads, 4)
     jacobi_round_kernel(float* __restrict__ x_all, int kp, int rnd, int sweep, int* __restrict__ flags, int batch,
-                        float tol) {
+                        float tol, int max_sweeps) {
   __shared__ __align__(16) float xc[kJChunk][kJw + 4];
   __shared__ float gs[kJw][kJw + 1];
   __shared__ float gs2[kJw][kJw + 1];
@@ -299,6 +314,17 @@ __global__ void __launch_bounds__(kJThreads, 4)
   } else {
     P = (rnd + pi) % m;
     Qb = (rnd - pi + m) % m;
+  }
+  // A pair found converged stays converged until one of its blocks is rotated with another
+  // partner: block stamps (round of the last rotation) and pair stamps (round found converged)
+  // let it skip the Gram.
+  int* bstamp = flags + max_sweeps * batch + b * nb;
+  int* pstamp = flags + max_sweeps * batch + batch * nb + static_cast<size_t>(b) * nb * nb;
+  const int now = sweep * m + rnd + 1;
+  const int pq = min(P, Qb) * nb + max(P, Qb);
+  {
+    const int ps = pstamp[pq];
+    if (ps > 0 && bstamp[P] < ps && bstamp[Qb] < ps) return;
   }
   float* x = x_all + static_cast<size_t>(b) * kp * kp;
   auto col_ptr = [&](int c) { return x + static_cast<size_t>(c < kJb ? P * kJb + c : Qb * kJb + c - kJb) * kp; };
@@ -366,8 +392,15 @@ __global__ void __launch_bounds__(kJThreads, 4)
   __syncthreads();
   off = 0.f;
   for (int w = 0; w < kJThreads / 32; ++w) off = fmaxf(off, red[w]);
-  if (!(off > tol)) return;  // uniform across the CTA
-  if (tid == 0) flags[sweep * batch + b] = 1;
+  if (!(off > tol)) {  // uniform across the CTA
+    if (tid == 0) pstamp[pq] = now;
+    return;
+  }
+  if (tid == 0) {
+    flags[sweep * batch + b] = 1;
+    bstamp[P] = now;
+    bstamp[Qb] = now;
+  }
   // ---- one cyclic sweep of two-sided Jacobi on G (31 rounds of 16 disjoint rotations).
   // Thread t owns the 2x2 block (pair p = t/16, pair q = t%16) of the round's pairing and
   // writes G'_pq = R_p^T G_pq R_q from the previous G (double buffer: one barrier per
@@ -562,18 +595,27 @@ __global__ void __launch_bounds__(kFinThreads)
     for (int j = tid; j < R; j += kFinThreads) sv_all[static_cast<size_t>(b) * R + j] = static_cast<float>(key[j]);
 }
 
-int chol_panel(int k) { return k <= 512 ? 32 : k <= 1100 ? 16 : 8; }
-size_t chol_smem(int k) { return static_cast<size_t>(k) * (chol_panel(k) + 1) * sizeof(double); }
 
 }  // namespace
 
 void chol_batched(double* g, int k, int batch, double shift_rel, double* lo, float* lf, int* perm, cudaStream_t st) {
-  require(k >= 1 && k <= 2048, KVP_ERR_PARAMETER, "chol: k out of range");
-  const size_t smem = chol_smem(k);
-  require(smem <= 200 * 1024, KVP_ERR_PARAMETER, "chol: k too large for the panel");
-  KVP_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  chol_kernel<<<batch, kCholThreads, smem, st>>>(g, k, chol_panel(k), shift_rel, lo, lf, perm);
+  require(k >= 1, KVP_ERR_PARAMETER, "chol: k out of range");
+  KVP_CUDA(cudaMemsetAsync(lo, 0, sizeof(double) * batch * k * k, st));
+  chol_prep_kernel<<<batch, 256, 0, st>>>(g, k, shift_rel, perm);
   KVP_LAUNCHED();
+  for (int j0 = 0; j0 < k; j0 += kCp) {
+    chol_panel_kernel<<<batch, 256, 0, st>>>(g, k, j0, lo);
+    KVP_LAUNCHED();
+    const int n = k - j0 - kCp;
+    if (n <= 0) break;
+    const int nt = (n + kCp - 1) / kCp;
+    chol_update_kernel<<<dim3(nt * (nt + 1) / 2, batch), 256, 0, st>>>(g, k, j0, lo);
+    KVP_LAUNCHED();
+  }
+  if (lf) {
+    chol_lf_kernel<<<dim3(cdiv(static_cast<long>(k) * k, 256), batch), 256, 0, st>>>(lo, k, lf);
+    KVP_LAUNCHED();
+  }
 }
 
 template <typename T>
@@ -601,6 +643,10 @@ void trsm_rows_f64(const float* y, float* q, int n, int k, int batch, const doub
 }
 
 int jacobi_kp(int k) { return (k + kJChunk - 1) / kJChunk * kJChunk; }
+size_t jacobi_ws_ints(int k, int batch, int max_sweeps) {
+  const size_t nb = static_cast<size_t>(jacobi_kp(k)) / kJb;
+  return static_cast<size_t>(max_sweeps) * batch + batch * nb + batch * nb * nb;
+}
 
 void jacobi_eig(const double* lo, int k, int batch, int R, float* x, int* flags, int max_sweeps, float tol,
                 double rank_tol, float* us, float* ui, float* sv, cudaStream_t st) {
@@ -608,11 +654,11 @@ void jacobi_eig(const double* lo, int k, int batch, int R, float* x, int* flags,
   require(kp <= 2 * kFinThreads, KVP_ERR_PARAMETER, "jacobi: k too large");
   lo_to_x_kernel<<<dim3(cdiv(static_cast<long>(kp) * kp, 256 * 8), batch), 256, 0, st>>>(lo, k, x, kp);
   KVP_LAUNCHED();
-  KVP_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * max_sweeps * batch, st));
+  KVP_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * jacobi_ws_ints(k, batch, max_sweeps), st));
   const int nb = kp / kJb;
   for (int s = 0; s < max_sweeps; ++s)
     for (int r = 0; r < nb - 1; ++r) {
-      jacobi_round_kernel<<<dim3(nb / 2, batch), kJThreads, 0, st>>>(x, kp, r, s, flags, batch, tol);
+      jacobi_round_kernel<<<dim3(nb / 2, batch), kJThreads, 0, st>>>(x, kp, r, s, flags, batch, tol, max_sweeps);
       KVP_LAUNCHED();
     }
   const size_t smem = 2 * kFinThreads * (sizeof(double) + sizeof(int));

@@ -16,7 +16,7 @@ layers = int(sys.argv[2]) if len(sys.argv) > 2 else 2
 cfg = CONFIGS[name]
 H, Hkv, D = cfg["geom"]
 torch.zeros(1).cuda()
-for rep in range(2):
+for rep in range(int(sys.argv[3]) if len(sys.argv) > 3 else 2):
     spec = EngineSpec(heads=H, kv_heads=Hkv, head_dim=D, layers=layers, batch=cfg["batch"],
                       visual_tokens=cfg["visual"], textual_tokens=cfg["textual"], decode_steps=4,
                       rank_k=cfg["rank"], rank_v=cfg["rank"], factor_init="compaction")
