@@ -154,6 +154,12 @@ int kvp_truncated_svd(const float* a, int32_t batch, int32_t T, int32_t W, int32
                       uint64_t seed, int32_t oversampling, int32_t power_iterations, float* left, float* right,
                       float* sv, void* stream);
 
+/* quantize_roundtrip (bindings/module.cpp:223-230): quantize_4bit + dequantize
+ * (quantize.cpp:10-54) of a row-major f64 matrix, groups of group_size rows per column;
+ * a, out [dev].  Bit-identical to the reference. */
+int kvp_quantize_roundtrip(const double* a, int64_t rows, int64_t cols, int64_t group_size, double* out,
+                           void* stream);
+
 /* gaussian_matrix (linalg.hpp:55-58): rows x cols N(0,1) draws of the Philox
  * stream (seed, stream_id) (rng.hpp:15-98), row-major, dtype f32 or f64 [dev]. */
 int kvp_gaussian_matrix(int64_t rows, int64_t cols, uint64_t seed, uint64_t stream_id, int32_t dtype, void* out,

@@ -270,6 +270,15 @@ def flops_partial_decompress(tokens, width, ratios, ranks):
     return fl.value, red.value
 
 
+def quantize_roundtrip(a, group_size=64):
+    """dequantize(quantize_4bit(a, group_size)) (quantize.cpp:10-54), double."""
+    a = _f64(a)
+    out = np.zeros_like(a)
+    _check(lib().kvref_quantize_roundtrip(C.c_size_t(a.shape[0]), C.c_size_t(a.shape[1]), _dp(a),
+                                          C.c_size_t(group_size), _dp(out)))
+    return out
+
+
 def compression_ratio(tokens, width, rank):
     out = C.c_double()
     _check(lib().kvref_compression_ratio(C.c_size_t(tokens), C.c_size_t(width), C.c_size_t(rank), C.byref(out)))

@@ -19,6 +19,7 @@
 #include "kvpack/harness.hpp"
 #include "kvpack/importance.hpp"
 #include "kvpack/linalg.hpp"
+#include "kvpack/quantize.hpp"
 #include "kvpack/snapshot.hpp"
 
 using namespace kvpack;
@@ -428,6 +429,12 @@ int kvref_flops_partial_decompress(std::size_t tokens, std::size_t width, std::s
         *flops = c.flops;
         *reduction = c.reduction;
     });
+}
+
+// quantize_roundtrip (module.cpp:223-230): dequantize(quantize_4bit(a, group_size)), double.
+int kvref_quantize_roundtrip(std::size_t rows, std::size_t cols, const double* a, std::size_t group_size,
+                             double* out) {
+    return guarded([&] { mat_out(dequantize(quantize_4bit(mat_in<double>(rows, cols, a), group_size)), out); });
 }
 
 int kvref_compression_ratio(std::size_t tokens, std::size_t width, std::size_t rank, double* out) {

@@ -151,6 +151,7 @@ SIGNATURES = {
     "kvp_cache_get_importance": (C.c_int, [_P, _P, _P]),
     "kvp_cache_shape": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "kvp_cache_set_counters": (C.c_int, [_P, C.c_uint64, C.c_uint64]),
+    "kvp_quantize_roundtrip": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, _P, _P]),
     "kvp_cache_block_info": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P]),
     "kvp_cache_block_get": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P, _P, _P]),
     "kvp_cache_tail_get": (C.c_int, [_P, C.c_int32, C.c_int32, _P, _P, _P]),

@@ -236,11 +236,6 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) qdots_kernel
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / LPH, gl = lane % LPH;
   const int H = p.s.H, W = p.s.Hkv * D;
-  if ((a.pf & 1) && threadIdx.x == 0) {  // core's left_k for instance b -> L2 (independent of q)
-    const long blocks = static_cast<long>(p.ntiles) * p.kpk;
-    const unsigned char* base = a.left_k_packed + static_cast<long>(a.inst0 + b) * blocks * kStageBytes;
-    for (long i = g; i < blocks; i += p.s.Hkv) bulk_prefetch_l2(base + i * kStageBytes, kStageBytes);
-  }
   griddep_wait();               // q (and the new k, v) come from the projection GEMM
   griddep_launch_dependents();  // core may start its q-independent prologue and left_k stream
   if (p.split && g == 0 && threadIdx.x == 0) a.ws_count[b] = 0u;  // core's per-instance barrier (after its wait)
@@ -419,13 +414,6 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) vsum_kernel(
   // triggered this launch) do not depend on core: the first batch is in flight
   // while core finishes.  The weights U / p_tail are core's output.
   issue(r0);
-  if ((a.pf & 16) && a.pf_next && threadIdx.x == 0) {  // the following kernel's operand -> L2
-    const size_t nblk = static_cast<size_t>(gridDim.x) * gridDim.y, me = static_cast<size_t>(b) * gridDim.x + g;
-    const size_t share = (a.pf_next_bytes / nblk + 65535) & ~static_cast<size_t>(65535);
-    const size_t lo = me * share, hi = min(a.pf_next_bytes & ~static_cast<size_t>(15), lo + share);
-    for (size_t o = lo; o < hi; o += 65536)
-      bulk_prefetch_l2(static_cast<const unsigned char*>(a.pf_next) + o, static_cast<uint32_t>(hi - o < 65536 ? hi - o : 65536));
-  }
   griddep_wait();
   if (p.split) {  // U = sum of the token chunks' partials (each already scaled by its softmax correction)
     const int C = p.s.cluster;
@@ -552,22 +540,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         bulk_load(smem + L.phi, reinterpret_cast<const unsigned char*>(a.ws_pimg) + static_cast<size_t>(b) * pbytes,
                   pbytes, &bars[kPopReady]);
       };
-      if (a.pf & 2) {  // my left_v tiles -> L2 while left_k streams (they follow the S phase)
-        const long g0 = static_cast<long>(a.inst0 + b) * p.ntiles + it.tile0;
-        const unsigned char* src = a.left_v_packed + g0 * p.vpanels_st * static_cast<long>(kStageBytes);
-        const long bytes = static_cast<long>(it.tiles) * p.vpanels_st * kStageBytes;
-        for (long o = 0; o < bytes; o += kRing) bulk_prefetch_l2(src + o, static_cast<uint32_t>(bytes - o < kRing ? bytes - o : kRing));
-      }
-      if (a.pf & 12) {  // vsum's value basis / tail rows of this instance, my 1/C share -> L2
-        const long W = static_cast<long>(p.s.Hkv) * p.s.D;
-        auto share = [&](const __nv_bfloat16* base, long bytes) {
-          const long per = ((bytes + C - 1) / C + 15) & ~15L, lo = c * per, hi = min(bytes, lo + per) & ~15L;
-          for (long o = lo; o < hi; o += 65536)
-            bulk_prefetch_l2(reinterpret_cast<const unsigned char*>(base) + o, static_cast<uint32_t>(hi - o < 65536 ? hi - o : 65536));
-        };
-        if (a.pf & 4) share(a.right_v + static_cast<long>(b) * p.s.rank_v * W, 2L * p.s.rank_v * W);
-        if (a.pf & 8) share(a.tail_v + static_cast<long>(b) * p.s.tail_cap * W, 2L * n_tail * W);
-      }
       bool p_loaded = false;
       for (int i = 0; i < it.total; ++i) {
         if (i == NS) {  // the ring is full: the MMAs that free it need P
@@ -1085,14 +1057,6 @@ void bind_workspace(const FusedPlan& p, FusedArgs& a, void* ws) {
 
 // Programmatic dependent launch of the three decode kernels (each waits with
 // griddepcontrol.wait before reading its predecessor's output).  KVP_PDL=0 turns it off.
-int pf_mask() {
-  static const int m = [] {
-    const char* e = std::getenv("KVP_PF");
-    return e == nullptr ? 0 : std::atoi(e);
-  }();
-  return m;
-}
-
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("KVP_PDL");
@@ -1414,7 +1378,6 @@ extern "C" int kvp_decode_fused(const kvp_fused_desc* d, void* stream) {
     a.ctx_bf16 = d->context_bf16;
     bind_workspace(p, a, ws);
     a.trace = g_trace;
-    a.pf = pf_mask();
     launch_fused(p, a, st);
   });
 }

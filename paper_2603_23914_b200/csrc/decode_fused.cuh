@@ -59,12 +59,6 @@ struct FusedArgs {
   float* ws_stats;
   unsigned* ws_count;
   unsigned long long* trace;     // debug: per-CTA phase timestamps [grid][16] (nullable)
-  // L2 prefetch of the next phase's bytes (cp.async.bulk.prefetch.L2), issued by a phase whose own
-  // stream leaves HBM idle: bit 0 qdots -> core's left_k, bit 1 core -> its own left_v, bit 2 core ->
-  // vsum's right_v, bit 3 core -> vsum's tail_v, bit 4 vsum -> pf_next (the following kernel's operand)
-  int pf;
-  const void* pf_next;
-  size_t pf_next_bytes;
 };
 
 struct FusedPlan {
@@ -100,7 +94,6 @@ FusedShape resolve_fused_shape(FusedShape s);
 void bind_workspace(const FusedPlan& p, FusedArgs& a, void* ws);
 size_t packed_left_bytes(int batch, int n, int rank);
 void pack_left(const void* src, long ld, int batch, int n, int rank, void* dst, cudaStream_t st);
-int pf_mask();  // KVP_PF: default L2-prefetch bits of FusedArgs::pf
 void launch_fused(const FusedPlan& p, const FusedArgs& a, cudaStream_t st);
 // The three launches separately (engine pipelining across instance groups).
 void launch_qdots(const FusedPlan& p, const FusedArgs& a, cudaStream_t st);

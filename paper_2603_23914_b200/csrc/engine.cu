@@ -294,11 +294,6 @@ FusedArgs fused_args(kvp_engine* e, int l, bool append_kv) {
   a.vtier = e->vtier ? e->vtier + static_cast<size_t>(lidx) * e->B * e->n : nullptr;
   bind_workspace(e->plan, a, e->fused_ws);
   a.trace = nullptr;
-  a.pf = pf_mask();
-  // vsum -> the W_o GEMM's weights
-  a.pf_next = e->use_cublas ? static_cast<const void*>(e->wo + lidx * e->HD * e->HD)
-                            : static_cast<const void*>(e->wo_pk + lidx * e->wo_pk_bytes);
-  a.pf_next_bytes = e->use_cublas ? sizeof(__nv_bfloat16) * static_cast<size_t>(e->HD) * e->HD : e->wo_pk_bytes;
   return a;
 }
 

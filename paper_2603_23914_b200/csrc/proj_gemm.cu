@@ -50,7 +50,7 @@ template <int NB>
 __global__ void __launch_bounds__(kPThreads, 1)
     proj_gemm_kernel(const unsigned char* __restrict__ wpk, const __grid_constant__ CUtensorMap map_x, int N, int B,
                      int kst, int stages, void* __restrict__ out, int ldo, int out_bf16, float* __restrict__ ws,
-                     unsigned* __restrict__ counters, int maxseg, int dbg, unsigned long long* __restrict__ trace) {
+                     unsigned* __restrict__ counters, int maxseg, unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(1024) unsigned char psmem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(psmem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t kXBytes = NB * 128;               // one 64-deep x tile (NB token rows x 128 B)
@@ -100,20 +100,20 @@ __global__ void __launch_bounds__(kPThreads, 1)
       // weights of the first ring before the dependency wait; x (the previous kernel's output) after
       const long pre = s1 - s0 < stages ? s1 - s0 : stages;
       for (long j = 0; j < pre; ++j) {
-        mbar_expect_tx(&full[j], (dbg & 2) ? 2 * kWBlock : kStage);
+        mbar_expect_tx(&full[j], kStage);
         bulk_load(smem + j * kStage, wpk + (s0 + j) * static_cast<long>(2 * kWBlock), 2 * kWBlock, &full[j]);
       }
       stamp(2);
       griddep_wait();
       stamp(3);
-      for (long j = 0; j < pre && !(dbg & 2); ++j) load_x(smem + j * kStage, s0 + j, &full[j]);
+      for (long j = 0; j < pre; ++j) load_x(smem + j * kStage, s0 + j, &full[j]);
       for (long j = pre; j < s1 - s0; ++j) {
         const int st = static_cast<int>(j % stages);
         mbar_wait(&empty[st], static_cast<uint32_t>(((j / stages) - 1) & 1));
         unsigned char* dst = smem + st * kStage;
-        mbar_expect_tx(&full[st], (dbg & 2) ? 2 * kWBlock : kStage);
+        mbar_expect_tx(&full[st], kStage);
         bulk_load(dst, wpk + (s0 + j) * static_cast<long>(2 * kWBlock), 2 * kWBlock, &full[st]);
-        if (!(dbg & 2)) load_x(dst, s0 + j, &full[st]);
+        load_x(dst, s0 + j, &full[st]);
       }
       griddep_launch_dependents();
     }
@@ -137,8 +137,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
           const uint32_t sa = base + st * kStage, sb = sa + 2 * kWBlock;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            if (!(dbg & 1))
-              mma_bf16(d, smem_desc(sa + (kk >> 2) * kWBlock + (kk & 3) * 2048, kWBlock / 2, 1024, kSwizzle128B),
+            mma_bf16(d, smem_desc(sa + (kk >> 2) * kWBlock + (kk & 3) * 2048, kWBlock / 2, 1024, kSwizzle128B),
                        smem_desc(sb + (kk >> 2) * kXBytes + (kk & 3) * 32, 16, 1024, kSwizzle128B), idesc,
                        (q != s || kk != 0) ? 1u : 0u);
           mma_commit(&empty[st]);
@@ -251,10 +250,6 @@ __global__ void pack_weight_kernel(const __nv_bfloat16* __restrict__ w, int K, i
 }
 
 unsigned long long* g_ptrace = nullptr;
-int dbg_flags() {
-  static const int f = std::getenv("KVP_PG_DBG") ? std::atoi(std::getenv("KVP_PG_DBG")) : 0;
-  return f;
-}
 
 template <int NB>
 void launch_nb(const ProjGemm& g, const unsigned char* wpk, const CUtensorMap& mx, void* out, int ldo, bool out_bf16,
@@ -276,10 +271,9 @@ void launch_nb(const ProjGemm& g, const unsigned char* wpk, const CUtensorMap& m
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  static const bool pdl = std::getenv("KVP_PG_PDL") == nullptr || std::atoi(std::getenv("KVP_PG_PDL")) != 0;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = 1;
   KVP_CUDA(cudaLaunchKernelEx(&cfg, proj_gemm_kernel<NB>, wpk, mx, g.N, g.B, g.kst, g.stages, out, ldo,
-                              out_bf16 ? 1 : 0, g.ws, g.counters, g.maxseg, dbg_flags(), g_ptrace));
+                              out_bf16 ? 1 : 0, g.ws, g.counters, g.maxseg, g_ptrace));
   KVP_LAUNCHED();
 }
 
@@ -307,12 +301,10 @@ ProjGemm proj_gemm_plan(int K, int N, int B, int sms) {
   g.kst = (K + 127) / 128;
   const long S = static_cast<long>((N + 127) / 128) * g.kst;
   g.grid = static_cast<int>(std::min<long>(sms, S));
-  if (const char* e = std::getenv("KVP_PG_GRID")) g.grid = std::max(1, std::min<int>(g.grid, std::atoi(e)));
   const long per = S / g.grid;  // every CTA holds >= per stages, so a tile spans <= ceil(kst/per) + 1 CTAs
   g.maxseg = static_cast<int>((g.kst + per - 1) / per + 1);
   const uint32_t stage = 2 * kWBlock + 2 * static_cast<uint32_t>(g.nb) * 128;
   g.stages = std::min<int>(kPMaxStages, static_cast<int>((220u * 1024u) / stage));
-  if (const char* e = std::getenv("KVP_PG_STAGES")) g.stages = std::max(2, std::min(g.stages, std::atoi(e)));
   g.ws_bytes = sizeof(float) * static_cast<size_t>((N + 127) / 128) * g.maxseg * g.nb * 128 +
                sizeof(unsigned) * static_cast<size_t>((N + 127) / 128);
   return g;

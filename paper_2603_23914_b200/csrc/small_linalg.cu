@@ -35,9 +35,10 @@ namespace {
 
 // ---------------------------------------------------------------------------
 // Batched Cholesky, fp64, blocked right-looking over 32-column panels, two launches per panel:
-//   chol_panel_kernel  (one CTA per matrix): factor the 32 x 32 diagonal block in shared memory
-//                      (one warp, lane = row), then the panel below it, L_iJ = S_iJ L_JJ^-T
-//                      (one thread per row, forward substitution in registers);
+//   chol_panel_kernel  (64-row chunks of the panel per CTA): factor the 32 x 32 diagonal block in
+//                      shared memory (one warp, lane = row; every chunk's CTA redundantly), then its
+//                      rows of the panel, L_iJ = S_iJ L_JJ^-T (one thread per row, forward
+//                      substitution in registers);
 //   chol_update_kernel (one CTA per 32 x 32 tile of the trailing lower triangle, every matrix):
 //                      S_im -= L_iJ L_mJ^T.
 //   s    : [batch][k][k] symmetric input (lower triangle read), overwritten by the updates
@@ -73,13 +74,16 @@ __global__ void chol_prep_kernel(double* __restrict__ s_all, int k, double shift
   for (int i = tid; i < k; i += blockDim.x) S[static_cast<size_t>(i) * k + i] += shift;
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(64)
     chol_panel_kernel(const double* __restrict__ s_all, int k, int j0, double* __restrict__ lo_all) {
   __shared__ double D[kCp][kCp + 1];
-  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
   const double* S = s_all + static_cast<size_t>(b) * k * k;
   double* lo = lo_all + static_cast<size_t>(b) * k * k;
   const int nb = min(kCp, k - j0);
+  // rows of the panel below are split over gridDim.x CTAs; each factors the diagonal block itself
+  const int rows_per = (k - j0 - nb + gridDim.x - 1) / gridDim.x;
+  const int rbeg = j0 + nb + blockIdx.x * rows_per, rend = min(k, rbeg + rows_per);
   for (int e = tid; e < kCp * kCp; e += blockDim.x) {
     const int r = e / kCp, c = e % kCp;
     D[r][c] = (r < nb && c <= r) ? S[static_cast<size_t>(j0 + r) * k + j0 + c] : 0.0;
@@ -103,12 +107,13 @@ __global__ void __launch_bounds__(256)
     }
   }
   __syncthreads();
-  for (int e = tid; e < nb * nb; e += blockDim.x) {
-    const int r = e / nb, c = e % nb;
-    if (c <= r) lo[static_cast<size_t>(j0 + r) * k + j0 + c] = D[r][c];
-  }
+  if (blockIdx.x == 0)
+    for (int e = tid; e < nb * nb; e += blockDim.x) {
+      const int r = e / nb, c = e % nb;
+      if (c <= r) lo[static_cast<size_t>(j0 + r) * k + j0 + c] = D[r][c];
+    }
   // panel below: row i solves x L_JJ^T = S[i][J]
-  for (int i = j0 + nb + tid; i < k; i += blockDim.x) {
+  for (int i = rbeg + tid; i < rend; i += blockDim.x) {
     double x[kCp];
     const double* srow = S + static_cast<size_t>(i) * k + j0;
 #pragma unroll
@@ -604,7 +609,8 @@ void chol_batched(double* g, int k, int batch, double shift_rel, double* lo, flo
   chol_prep_kernel<<<batch, 256, 0, st>>>(g, k, shift_rel, perm);
   KVP_LAUNCHED();
   for (int j0 = 0; j0 < k; j0 += kCp) {
-    chol_panel_kernel<<<batch, 256, 0, st>>>(g, k, j0, lo);
+    const int below = k - j0 - kCp;
+    chol_panel_kernel<<<dim3(below > 0 ? cdiv(below, 64) : 1, batch), 64, 0, st>>>(g, k, j0, lo);
     KVP_LAUNCHED();
     const int n = k - j0 - kCp;
     if (n <= 0) break;

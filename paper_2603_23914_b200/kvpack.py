@@ -8,9 +8,11 @@ Arrays are copied, never aliased (module.cpp:6, 29-47).  The factorisation,
 the importance EMA and the tier assignment run on the GPU through
 libkvp_b200.so; compression_ratio and partial_decompress_flops are the
 reference's closed-form integer/f64 accounting and stay on the host.
+quantize_roundtrip (the 4-bit groupwise store's round trip) runs on the GPU,
+bit-identical to the reference.
 
-Not mirrored (outside this path): quantize_roundtrip (the
-4-bit hybrid store) and run_simulation (the INI-driven harness).
+Not mirrored (outside this path): run_simulation (the INI-driven
+harness).
 """
 from __future__ import annotations
 
@@ -25,6 +27,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "__version__",
+    "quantize_roundtrip",
     "assign_groups",
     "compression_ratio",
     "ema_update",
@@ -210,3 +213,24 @@ def assign_groups(scores, ratios, ranks):
     torch.cuda.synchronize()
     t = tier.cpu().numpy()
     return [np.flatnonzero(t == f).tolist() for f in range(len(ratios))]
+
+
+def quantize_roundtrip(a, group_size=64):
+    """4-bit groupwise quantize + dequantize (module.cpp:223-230, quantize.cpp:10-54):
+    per column, groups of ``group_size`` rows share a min and a scale (max - min) / 15;
+    per-element error <= (group max - group min) / 30.  Bit-identical to the reference."""
+    m = _matrix(a)
+    group_size = int(group_size)
+    if group_size < 1:
+        raise ValueError("quantize_4bit: group_size must be >= 1")
+    if not np.all(np.isfinite(m)):
+        raise ValueError("quantize_4bit: matrix contains non-finite values")
+    rows, cols = m.shape
+    if rows == 0 or cols == 0:
+        return m.copy()
+    torch = _torch()
+    dev = torch.as_tensor(m, dtype=torch.float64, device="cuda").contiguous()
+    out = torch.empty_like(dev)
+    capi.call("kvp_quantize_roundtrip", dev.data_ptr(), rows, cols, group_size, out.data_ptr(), None)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()

@@ -147,3 +147,43 @@ def test_assign_groups_partition():  # test_smoke.py:72-81
     assert [len(m) for m in masks] == [3, 3, 4]
     assert sorted(i for m in masks for i in m) == list(range(10))
     assert 0 in masks[0] and 8 in masks[2]
+
+
+def test_oracle_quantize_roundtrip_bound():  # test_smoke.py:83-91 against the compiled reference
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(6)
+    a = rng.uniform(-2.0, 2.0, size=(128, 16))
+    out = ref.quantize_roundtrip(a, 32)
+    for j in range(a.shape[1]):
+        for g in range(0, a.shape[0], 32):
+            block = a[g:g + 32, j]
+            assert np.abs(out[g:g + 32, j] - block).max() <= (block.max() - block.min()) / 30.0 + 1e-12
+
+
+@pytest.mark.gpu
+def test_quantize_roundtrip_bit_exact_with_reference():
+    # test_smoke.py:83-91 plus edge cases (quantize.cpp:10-54): ragged last group, group_size 1,
+    # constant groups (zero scale), +-0 ties, a single row; bit-identical to the compiled reference
+    _gpu()
+    from oracle import ref
+    rng = np.random.default_rng(6)
+    a = rng.uniform(-2.0, 2.0, size=(128, 16))
+    out = kvpack.quantize_roundtrip(a, group_size=32)
+    for j in range(a.shape[1]):
+        for g in range(0, a.shape[0], 32):
+            block = a[g:g + 32, j]
+            assert np.abs(out[g:g + 32, j] - block).max() <= (block.max() - block.min()) / 30.0 + 1e-12
+    cases = [(a, 32), (rng.standard_normal((67, 9)), 16), (rng.standard_normal((5, 3)), 1),
+             (np.r_[np.full((8, 4), 0.5), rng.standard_normal((9, 4))], 8),
+             (np.array([[0.0, -0.0], [-0.0, 0.0], [1.0, -1.0]]), 2), (rng.standard_normal((1, 7)), 64),
+             (rng.standard_normal((300, 40)) * 1e3, 64)]
+    for m, gs in cases:
+        got = kvpack.quantize_roundtrip(m, group_size=gs)
+        want = ref.quantize_roundtrip(m, gs)
+        assert np.array_equal(got.view(np.int64), want.view(np.int64)), gs
+    with pytest.raises(ValueError):
+        kvpack.quantize_roundtrip(a, group_size=0)
+    with pytest.raises(ValueError):
+        kvpack.quantize_roundtrip(np.array([[np.nan]]))
