@@ -420,9 +420,14 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) vsum_kernel(
     for (int i = threadIdx.x; i < PER_KV * rows; i += kStreamThreads) {
       const int y = i / rows, r = i % rows, h = g * PER_KV + y;
       float u = 0.f;
-      if (r < rv)
-        for (int cc = 0; cc < C; ++cc) u += __ldcg(&a.ws_u[((static_cast<long>(b) * C + cc) * H + h) * rv + r]);
-      else
+      if (r < rv) {
+        // the C partial loads are independent: unrolled so they are all in flight at once (a rolled
+        // loop serialises C L2 round trips on vsum's critical path)
+        const float* up = a.ws_u + (static_cast<long>(b) * C * H + h) * rv + r;
+        const long cs = static_cast<long>(H) * rv;
+#pragma unroll 8
+        for (int cc = 0; cc < C; ++cc) u += __ldcg(up + cc * cs);
+      } else
         u = a.ws_tail[(static_cast<long>(b) * H + h) * p.s.tail_cap + (r - rv)];
       wts[y * wstride + r] = u;
     }
