@@ -424,9 +424,9 @@ void compact_visual(kvp_engine* e) {
   KVP_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const size_t budget = std::min<size_t>(40ull << 30, free_b / 4);
   const int chunk = std::max(1, std::min<int>(e->L, static_cast<int>(budget / (per_layer * sizeof(float)))));
-  // layers in flight: up to 4, as the device memory left after the staging allows (~2x a layer's
+  // layers in flight: up to 8, as the device memory left after the staging allows (~2x a layer's
   // fp32 inputs of SVD scratch per lane: bf16 hi/lo of A, sketches, B^T in fp32 and fp64)
-  constexpr int kMaxLanes = 4;
+  constexpr int kMaxLanes = 8;
   const size_t lane_bytes = 2 * per_layer * sizeof(float);
   const size_t left_after = free_b > static_cast<size_t>(chunk) * per_layer * sizeof(float)
                                 ? free_b - static_cast<size_t>(chunk) * per_layer * sizeof(float)
