@@ -346,6 +346,22 @@ cudaMemPool_t svd_pool() {
   return pool;
 }
 
+// Maps `bytes` into the compaction pool ahead of a timed region: allocated in 1 GB pieces and
+// freed at once (the pool keeps its pages until svd_pool_trim).
+void svd_pool_reserve(size_t bytes, cudaStream_t st) {
+  std::vector<void*> ps;
+  for (size_t done = 0; done < bytes; done += (1ull << 30)) {
+    void* p = nullptr;
+    if (cudaMallocFromPoolAsync(&p, std::min<size_t>(1ull << 30, bytes - done), svd_pool(), st) != cudaSuccess) {
+      (void)cudaGetLastError();  // best effort: the SVD grows the pool on demand
+      break;
+    }
+    ps.push_back(p);
+  }
+  for (void* p : ps) KVP_CUDA(cudaFreeAsync(p, st));
+  KVP_CUDA(cudaStreamSynchronize(st));
+}
+
 void svd_pool_trim() {
   std::lock_guard<std::recursive_mutex> lock(svd_mutex());
   cudaMemPoolTrimTo(svd_pool(), 0);

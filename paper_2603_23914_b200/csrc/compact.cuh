@@ -18,6 +18,8 @@ void randomized_svd_batched(cublasHandle_t blas, cudaStream_t stream, const floa
 // c: fp32 [batch][M][ldc] (ldc 0 = n) with M = trans_a ? W : T, K = trans_a ? T : W; accumulate: c += A X.
 // Returns the compaction scratch pool's idle pages to the device.
 void svd_pool_trim();
+// Maps `bytes` into the compaction scratch pool ahead of a timed region.
+void svd_pool_reserve(size_t bytes, cudaStream_t st);
 int range_gemm_npad();
 // bf16 [batch][rows][cols] row-major as a 3-D tensor map, box {64, box_rows, 1}, 128-byte swizzle,
 // out-of-bounds rows zero-filled.

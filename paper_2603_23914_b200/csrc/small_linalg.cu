@@ -333,20 +333,26 @@ __global__ void __launch_bounds__(kJThreads, 4)
   }
   float* x = x_all + static_cast<size_t>(b) * kp * kp;
   auto col_ptr = [&](int c) { return x + static_cast<size_t>(c < kJb ? P * kJb + c : Qb * kJb + c - kJb) * kp; };
-  auto load_chunk = [&](int r0) {
-    // lane -> column, warp -> 8 consecutive rows (one 32-byte sector per lane; conflict-free stores)
+  // Chunk staging, software-pipelined: the next 64-row chunk's global loads are issued into
+  // registers before the current chunk is computed, so their latency hides behind the FMAs.
+  // lane -> column, warp -> 8 consecutive rows (one 32-byte sector per lane; conflict-free stores)
+  float4 pa, pb;
+  auto fetch_chunk = [&](int r0) {
     const int c = tid & 31, rr = (tid >> 5) * 8;
     const float* src = col_ptr(c) + r0 + rr;
-    const float4 a = *reinterpret_cast<const float4*>(src);
-    const float4 bq = *reinterpret_cast<const float4*>(src + 4);
-    xc[rr + 0][c] = a.x;
-    xc[rr + 1][c] = a.y;
-    xc[rr + 2][c] = a.z;
-    xc[rr + 3][c] = a.w;
-    xc[rr + 4][c] = bq.x;
-    xc[rr + 5][c] = bq.y;
-    xc[rr + 6][c] = bq.z;
-    xc[rr + 7][c] = bq.w;
+    pa = *reinterpret_cast<const float4*>(src);
+    pb = *reinterpret_cast<const float4*>(src + 4);
+  };
+  auto store_chunk = [&]() {
+    const int c = tid & 31, rr = (tid >> 5) * 8;
+    xc[rr + 0][c] = pa.x;
+    xc[rr + 1][c] = pa.y;
+    xc[rr + 2][c] = pa.z;
+    xc[rr + 3][c] = pa.w;
+    xc[rr + 4][c] = pb.x;
+    xc[rr + 5][c] = pb.y;
+    xc[rr + 6][c] = pb.z;
+    xc[rr + 7][c] = pb.w;
   };
   // ---- Gram G = X_P^T X_P: four row groups of 16 rows per 64-row chunk; inside a group
   // thread (ti, tj) owns the 4 x 4 tile G[4ti.., 4tj..] (two float4 shared loads per 16 FMA).
@@ -356,9 +362,11 @@ __global__ void __launch_bounds__(kJThreads, 4)
   double accd[4][4];
   for (int x = 0; x < 4; ++x)
     for (int y = 0; y < 4; ++y) accd[x][y] = 0.0;
+  fetch_chunk(0);
   for (int r0 = 0; r0 < kp; r0 += kJChunk) {
-    load_chunk(r0);
+    store_chunk();
     __syncthreads();
+    if (r0 + kJChunk < kp) fetch_chunk(r0 + kJChunk);
     float acc[4][4] = {};
 #pragma unroll 4
     for (int r = rg * 16; r < rg * 16 + 16; ++r) {
@@ -490,9 +498,11 @@ __global__ void __launch_bounds__(kJThreads, 4)
   // Thread (rr = tid/8, cg = tid%8) computes rows 2rr, 2rr+1 x columns 4cg..4cg+3.
   {
     const int rr = tid >> 3, cg = tid & 7;
+    fetch_chunk(0);
     for (int r0 = 0; r0 < kp; r0 += kJChunk) {
-      load_chunk(r0);
+      store_chunk();
       __syncthreads();
+      if (r0 + kJChunk < kp) fetch_chunk(r0 + kJChunk);
       float o[2][4] = {};
 #pragma unroll 2
       for (int mm = 0; mm < kJw; mm += 4) {
