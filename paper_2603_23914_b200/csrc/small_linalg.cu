@@ -39,7 +39,7 @@ namespace {
 //                      shared memory (one warp, lane = row; every chunk's CTA redundantly), then its
 //                      rows of the panel, L_iJ = S_iJ L_JJ^-T (one thread per row, forward
 //                      substitution in registers);
-//   chol_update_kernel (one CTA per 32 x 32 tile of the trailing lower triangle, every matrix):
+//   chol_update_kernel (one CTA per 64 x 64 tile of the trailing lower triangle, every matrix):
 //                      S_im -= L_iJ L_mJ^T.
 //   s    : [batch][k][k] symmetric input (lower triangle read), overwritten by the updates
 //   lo   : [batch][k][k] lower factor L (zeros above), g + shift = L L^T
@@ -77,6 +77,7 @@ __global__ void chol_prep_kernel(double* __restrict__ s_all, int k, double shift
 __global__ void __launch_bounds__(64)
     chol_panel_kernel(const double* __restrict__ s_all, int k, int j0, double* __restrict__ lo_all) {
   __shared__ double D[kCp][kCp + 1];
+  __shared__ double dinv[kCp];
   const int b = blockIdx.y, tid = threadIdx.x, lane = tid & 31;
   const double* S = s_all + static_cast<size_t>(b) * k * k;
   double* lo = lo_all + static_cast<size_t>(b) * k * k;
@@ -90,21 +91,32 @@ __global__ void __launch_bounds__(64)
   }
   __syncthreads();
   if (tid < 32) {
-    // lane = row r of the diagonal block; column c: pivot, scale, rank-1 update of the rows below
-    for (int c = 0; c < nb; ++c) {
-      const double piv = D[c][c];
-      const double l = piv > 0.0 ? sqrt(piv) : 0.0;
-      const double inv = piv > 0.0 ? 1.0 / l : 0.0;
-      __syncwarp();
-      if (lane > c && lane < nb) D[lane][c] *= inv;
-      if (lane == c) D[c][c] = l;
-      __syncwarp();
-      if (lane > c && lane < nb) {
-        const double lr = D[lane][c];
-        for (int q = c + 1; q <= lane; ++q) D[lane][q] = fma(-lr, D[q][c], D[lane][q]);
+    // lane = row r of the diagonal block, held in registers; column c: the pivot comes from lane c,
+    // rows below scale their entry and take the rank-1 update with the other rows' column-c
+    // entries by shuffle (fully unrolled: static register indices, no shared-memory round trips)
+    double row[kCp];
+#pragma unroll
+    for (int q = 0; q < kCp; ++q) row[q] = D[lane][q];
+#pragma unroll
+    for (int c = 0; c < kCp; ++c) {
+      if (c < nb) {
+        const double piv = __shfl_sync(0xffffffffu, row[c], c);
+        const double l = piv > 0.0 ? sqrt(piv) : 0.0;
+        const double inv = piv > 0.0 ? 1.0 / l : 0.0;
+        if (lane == c) row[c] = l;
+        else if (lane > c) row[c] *= inv;
+        const double lc = row[c];
+#pragma unroll
+        for (int q = c + 1; q < kCp; ++q) {
+          const double lq = __shfl_sync(0xffffffffu, lc, q);  // L[q][c]
+          if (lane >= q) row[q] = fma(-lc, lq, row[q]);
+        }
       }
-      __syncwarp();
     }
+#pragma unroll
+    for (int q = 0; q < kCp; ++q) D[lane][q] = (lane < nb && q <= lane) ? row[q] : 0.0;
+    const double dl = D[lane][lane];  // this lane's own store above
+    dinv[lane] = (lane < nb && dl > 0.0) ? 1.0 / dl : 0.0;
   }
   __syncthreads();
   if (blockIdx.x == 0)
@@ -123,7 +135,7 @@ __global__ void __launch_bounds__(64)
       if (c < nb) {
         double v = x[c];
         for (int t = 0; t < c; ++t) v = fma(-x[t], D[c][t], v);
-        x[c] = D[c][c] > 0.0 ? v / D[c][c] : 0.0;
+        x[c] = v * dinv[c];
       }
     }
     double* lrow = lo + static_cast<size_t>(i) * k + j0;
@@ -133,10 +145,12 @@ __global__ void __launch_bounds__(64)
   }
 }
 
-// Trailing update of the lower triangle below panel j0: one CTA per 32 x 32 tile (ta >= tb).
+// Trailing update of the lower triangle below panel j0: one CTA per 64 x 64 tile (ta >= tb),
+// thread -> 4 x 4 register tile, L rows staged in shared memory.
+constexpr int kCu = 64;
 __global__ void __launch_bounds__(256)
     chol_update_kernel(double* __restrict__ s_all, int k, int j0, const double* __restrict__ lo_all) {
-  __shared__ double La[kCp][kCp + 1], Lb[kCp][kCp + 1];
+  __shared__ double La[kCu][kCp + 1], Lb[kCu][kCp + 1];
   const int b = blockIdx.y, tid = threadIdx.x;
   const int r0 = j0 + kCp;
   const int tt = blockIdx.x;
@@ -144,28 +158,34 @@ __global__ void __launch_bounds__(256)
   while ((ta + 1) * (ta + 2) / 2 <= tt) ++ta;
   while (ta * (ta + 1) / 2 > tt) --ta;
   const int tb = tt - ta * (ta + 1) / 2;
-  const int i0 = r0 + ta * kCp, m0 = r0 + tb * kCp;
+  const int i0 = r0 + ta * kCu, m0 = r0 + tb * kCu;
   double* S = s_all + static_cast<size_t>(b) * k * k;
   const double* lo = lo_all + static_cast<size_t>(b) * k * k;
-  for (int e = tid; e < kCp * kCp; e += blockDim.x) {
+  for (int e = tid; e < kCu * kCp; e += blockDim.x) {
     const int r = e / kCp, c = e % kCp;
     La[r][c] = i0 + r < k ? lo[static_cast<size_t>(i0 + r) * k + j0 + c] : 0.0;
     Lb[r][c] = m0 + r < k ? lo[static_cast<size_t>(m0 + r) * k + j0 + c] : 0.0;
   }
   __syncthreads();
-  // thread -> row i0 + tid/8, columns m0 + (tid%8)*4 .. +3
-  const int r = tid >> 3, c4 = (tid & 7) * 4;
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 8
+  const int ri = (tid >> 4) * 4, ci = (tid & 15) * 4;
+  double acc[4][4] = {};
+#pragma unroll 4
   for (int t = 0; t < kCp; ++t) {
-    const double a = La[r][t];
-    for (int x = 0; x < 4; ++x) acc[x] = fma(a, Lb[c4 + x][t], acc[x]);
+    double av[4], bv[4];
+    for (int x = 0; x < 4; ++x) {
+      av[x] = La[ri + x][t];
+      bv[x] = Lb[ci + x][t];
+    }
+    for (int x = 0; x < 4; ++x)
+      for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
   }
-  const int i = i0 + r;
-  if (i >= k) return;
   for (int x = 0; x < 4; ++x) {
-    const int m = m0 + c4 + x;
-    if (m < k && m <= i) S[static_cast<size_t>(i) * k + m] -= acc[x];
+    const int i = i0 + ri + x;
+    if (i >= k) continue;
+    for (int y = 0; y < 4; ++y) {
+      const int m = m0 + ci + y;
+      if (m < k && m <= i) S[static_cast<size_t>(i) * k + m] -= acc[x][y];
+    }
   }
 }
 
@@ -624,7 +644,7 @@ void chol_batched(double* g, int k, int batch, double shift_rel, double* lo, flo
     KVP_LAUNCHED();
     const int n = k - j0 - kCp;
     if (n <= 0) break;
-    const int nt = (n + kCp - 1) / kCp;
+    const int nt = (n + kCu - 1) / kCu;
     chol_update_kernel<<<dim3(nt * (nt + 1) / 2, batch), 256, 0, st>>>(g, k, j0, lo);
     KVP_LAUNCHED();
   }
