@@ -32,13 +32,12 @@
 namespace kvp {
 namespace {
 
-
 // ---------------------------------------------------------------------------
 // Batched Cholesky, fp64, blocked right-looking over 32-column panels, two launches per panel:
 //   chol_panel_kernel  (64-row chunks of the panel per CTA): factor the 32 x 32 diagonal block in
-//                      shared memory (one warp, lane = row; every chunk's CTA redundantly), then its
-//                      rows of the panel, L_iJ = S_iJ L_JJ^-T (one thread per row, forward
-//                      substitution in registers);
+//                      registers (one warp, lane = row, shuffles; every chunk's CTA redundantly),
+//                      then its rows of the panel, L_iJ = S_iJ L_JJ^-T (one thread per row, forward
+//                      substitution in registers against the reciprocal diagonal);
 //   chol_update_kernel (one CTA per 64 x 64 tile of the trailing lower triangle, every matrix):
 //                      S_im -= L_iJ L_mJ^T.
 //   s    : [batch][k][k] symmetric input (lower triangle read), overwritten by the updates

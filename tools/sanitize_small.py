@@ -22,3 +22,5 @@ a = rng.standard_normal((256, 40)) @ rng.standard_normal((40, 512))
 left, right = kvpack.truncated_svd(a, 32, method="randomized", seed=1)
 print("svd rel err", float(np.linalg.norm(a - left @ right) / np.linalg.norm(a)),
       "orth", float(np.abs(right @ right.T - np.eye(32)).max()))
+q = kvpack.quantize_roundtrip(rng.standard_normal((67, 9)), group_size=16)
+print("quantize ok", q.shape)
