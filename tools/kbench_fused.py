@@ -32,11 +32,14 @@ def main():
     ap.add_argument("--cluster", type=int, default=0)
     ap.add_argument("--trace", action="store_true")
     ap.add_argument("--ld", type=int, default=0)
+    ap.add_argument("--batch", type=int, default=0, help="override the config's batch")
+    ap.add_argument("--streams", type=int, default=1, help="layers round-robin over this many streams")
     ap.add_argument("--tier", type=float, default=0.0,
                     help="two-tier values: first-group ratio r1 (the rest use a quarter of the value rank)")
     args = ap.parse_args()
     c = CONFIGS[args.config]
     B, H, Hkv, D, n, rk, rv, nt, cap = (c[k] for k in ("B", "H", "Hkv", "D", "n", "rk", "rv", "nt", "cap"))
+    B = args.batch or B
     W = Hkv * D
     ld = args.ld or (max(rk, rv) + 7) // 8 * 8
     dev = "cuda"
@@ -102,8 +105,21 @@ def main():
     s_cap = torch.cuda.Stream()
     with torch.cuda.stream(s_cap):
         g.capture_begin()
-        for L in layers:
-            capi.check(fn(C.byref(L["desc"]), s_cap.cuda_stream))
+        if args.streams > 1:
+            side = [torch.cuda.Stream() for _ in range(args.streams)]
+            ev0 = torch.cuda.Event()
+            ev0.record(s_cap)
+            for sd in side:
+                sd.wait_event(ev0)
+            for i, L in enumerate(layers):
+                capi.check(fn(C.byref(L["desc"]), side[i % args.streams].cuda_stream))
+            for sd in side:
+                e = torch.cuda.Event()
+                e.record(sd)
+                s_cap.wait_event(e)
+        else:
+            for L in layers:
+                capi.check(fn(C.byref(L["desc"]), s_cap.cuda_stream))
         g.capture_end()
     torch.cuda.synchronize()
     g.replay()
