@@ -72,7 +72,7 @@ constexpr int kStreamMinBlocks = KVP_STREAM_MINB;
 #endif
 
 struct Smem {
-  uint32_t ring, phi, plo, pt, pt2, stail, part, stats, imps, bars, tslot, total;
+  uint32_t ring, phi, plo, pt, pt2, stail, part, stats, imps, vts, bars, tslot, total;
   uint32_t uloc;  // late-phase alias over [phi, ...), valid once the U MMAs completed
   int uloc_stride;
 };
@@ -102,7 +102,8 @@ __host__ __device__ inline Smem smem_layout(const FusedPlan& p) {
   const uint32_t peer_bytes = p.split ? static_cast<uint32_t>(p.s.cluster) * 2 * np * 4 : 0;
   s.stats = s.part + (part_bytes > peer_bytes ? part_bytes : peer_bytes);
   s.imps = align_up(s.stats + (5 + 8) * np * 4, 16);
-  s.bars = align_up(s.imps + (p.chunk + p.tail_max) * 8, 8);
+  s.vts = s.imps + (p.chunk + p.tail_max) * 8;  // two-tier values: the chunk's tier flags (prefetched)
+  s.bars = align_up(s.vts + (p.nb2 > 0 ? p.chunk : 0), 8);
   s.tslot = s.bars + 40 * 8;
   s.total = align_up(s.tslot + 16, 1024);
   return s;
@@ -692,6 +693,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int j = i % it.n_tk, h = i / it.n_tk;
       stail[j * NP + h] = tg[static_cast<long>(h) * p.s.tail_cap + it.t_first + j];
     }
+    // the chunk's value-tier flags (written at the previous step's end): off the p-tile critical path
+    unsigned char* vts = smem + L.vts;
+    if (p.nb2 > 0) {
+      const unsigned char* vt = a.vtier + static_cast<long>(a.inst0 + b) * p.s.n_comp + it.c_first;
+      for (int i = tid; i < it.chunk_len; i += kComputeThreads) vts[i] = vt[i];
+    }
 
     // ---- local softmax: max over TMEM-resident S + my tail logits (no exponentials)
     const int qd = warp & 3;                 // TMEM lane quadrant this warp may access
@@ -744,8 +751,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row = qd * 32 + lane;  // token within the tile
       const bool valid = t * 128 + row < it.chunk_len;
       // two-tier values: a second-tier token's p goes to the second image only (U rows < rv2)
-      const bool tier2 = p.nb2 > 0 && valid &&
-                         a.vtier[static_cast<long>(a.inst0 + b) * p.s.n_comp + it.c_first + t * 128 + row] != 0;
+      const bool tier2 = p.nb2 > 0 && valid && vts[t * 128 + row] != 0;
       float sv[gcols];
       tld_row_hilo<ST, gcols>(tmem_row(static_cast<uint32_t>(t * NPW + gbase)), NP, sv);
 #pragma unroll
