@@ -234,136 +234,103 @@ __device__ __forceinline__ void tld_row_hilo(uint32_t taddr, int n, float (&v)[G
 }
 
 // ============================================================================
-// 1. qdots: rows = right_k (rank_k) then tail_k (n_tail) of every (kv head g,
-//    instance b) segment.  The work is a flat list of 8-row units over all
-//    segments, dealt in equal contiguous ranges to one wave of blocks (SMs x
-//    resident blocks), so every SM streams the same number of bytes (a grid of
-//    one block per segment left a quarter of the SMs one block short).  Each
-//    lane owns 8 columns of the g-slice; D/8 lanes span one row segment and
-//    reduce with shuffles.
+// 1. qdots: one block per (kv head g, instance b).  Rows = right_k (rank_k)
+//    then tail_k (n_tail); each lane owns 8 columns of the g-slice, D/8 lanes
+//    span one row segment and reduce with shuffles.
 // ============================================================================
 template <int PER_KV, int D>
 __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) qdots_kernel(const FusedPlan p, const FusedArgs a) {
   // A group of LPH = D/8 lanes covers one row segment (D bf16, one kv-head
-  // slice); each lane owns one 16-byte chunk.  A group takes units of 8
-  // consecutive rows: 8 independent 16-byte loads in flight per lane, one
-  // butterfly transpose-reduction (8 values over LPH lanes in log2(LPH) rounds),
-  // and the 8 results land as one 16-byte chunk of the swizzled P operand image.
+  // slice); each lane owns one 16-byte chunk and keeps its 8 query values in
+  // registers.  A group walks blocks of 8 consecutive rows: 8 independent
+  // 16-byte loads in flight per lane, one butterfly transpose-reduction
+  // (8 values over LPH lanes in log2(LPH) rounds), and the 8 results land as
+  // one 16-byte chunk of the swizzled P operand image (k = 8 consecutive ranks).
   constexpr int LPH = D / 8, GPW = 32 / LPH;  // lanes per row segment, groups per warp
+  const int g = blockIdx.x, b = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int grp = lane / LPH, gl = lane % LPH;
-  const int H = p.s.H, Hkv = p.s.Hkv, W = Hkv * D;
+  const int H = p.s.H, W = p.s.Hkv * D;
   griddep_wait();               // q (and the new k, v) come from the projection GEMM
   griddep_launch_dependents();  // core may start its q-independent prologue and left_k stream
+  if (p.split && g == 0 && threadIdx.x == 0) a.ws_count[b] = 0u;  // core's per-instance barrier (after its wait)
   const int n_tail = a.n_tail_dev ? *a.n_tail_dev : a.n_tail;
   const int rk = p.s.rank_k, rows = rk + n_tail;
+  const float scale = rsqrtf(static_cast<float>(D));
+  float qv[PER_KV][8];
+#pragma unroll
+  for (int y = 0; y < PER_KV; ++y)
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      qv[y][e] = a.q[static_cast<long>(b) * a.q_stride + (g * PER_KV + y) * D + gl * 8 + e] * scale;
+  const __nv_bfloat16* rkb = a.right_k + static_cast<long>(b) * rk * W + g * D + gl * 8;
+  const __nv_bfloat16* tkb = a.tail_k + static_cast<long>(b) * p.s.tail_cap * W + g * D + gl * 8;
+  if (a.append_kv) {  // the new token's k, v (this block's kv-head slice) -> tail row n_tail - 1
+    const float* src = a.q + static_cast<long>(b) * a.q_stride + static_cast<long>(H) * D + g * D;
+    const long row = static_cast<long>(b) * p.s.tail_cap + (n_tail - 1);
+    __nv_bfloat16* tk = const_cast<__nv_bfloat16*>(a.tail_k) + row * W + g * D;
+    __nv_bfloat16* tv = const_cast<__nv_bfloat16*>(a.tail_v) + row * W + g * D;
+    for (int i = threadIdx.x; i < D; i += kStreamThreads) {
+      tk[i] = __float2bfloat16_rn(src[i]);
+      tv[i] = __float2bfloat16_rn(src[W + i]);
+    }
+    if (g == 0 && threadIdx.x == 0 && a.importance)
+      a.importance[static_cast<long>(b) * a.imp_stride + p.s.n_comp + n_tail - 1] = 0.0;
+    __threadfence_block();
+    __syncthreads();
+  }
+  const int NP = p.np;
+  const bool st = p.stack;
+  const uint32_t plane = static_cast<uint32_t>(p.kpk) * NP * 128;  // bytes of one (hi or lo) operand
+  unsigned char* pimg = a.ws_pimg + static_cast<size_t>(b) * 2 * plane;
+  float* tout = a.ws_tail + static_cast<long>(b) * H * p.s.tail_cap;
+  // zero padding of the operand image: ranks >= rank_k of my heads; heads >= H (block g == 0)
+  for (int i = threadIdx.x; i < PER_KV * (p.kpk * 64 - rk); i += kStreamThreads) {
+    const int h = g * PER_KV + i / (p.kpk * 64 - rk), r = rk + i % (p.kpk * 64 - rk);
+    *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(st, NP, p.kpk, r >> 6, h, r & 63, false)) = __float2bfloat16_rn(0.f);
+    *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(st, NP, p.kpk, r >> 6, h, r & 63, true)) = __float2bfloat16_rn(0.f);
+  }
+  if (g == 0)
+    for (int i = threadIdx.x; i < (NP - H) * p.kpk * 64; i += kStreamThreads) {
+      const int h = H + i / (p.kpk * 64), r = i % (p.kpk * 64);
+      *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(st, NP, p.kpk, r >> 6, h, r & 63, false)) = __float2bfloat16_rn(0.f);
+      *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(st, NP, p.kpk, r >> 6, h, r & 63, true)) = __float2bfloat16_rn(0.f);
+    }
   // The appended row is this kernel's own write: the stream loop stops before it
   // (a non-coherent ld.global.nc of data written by the same kernel is undefined) and
   // its logits come from the fp32 source rounded to bf16, exactly the stored row.
   const int rows_ld = a.append_kv ? rows - 1 : rows;
   const int nblk = (rows_ld + 7) / 8;
-  const long units = static_cast<long>(Hkv) * p.s.batch * nblk;
-  const long u0 = units * blockIdx.x / gridDim.x, u1 = units * (blockIdx.x + 1) / gridDim.x;
-  const float scale = rsqrtf(static_cast<float>(D));
-  const int NP = p.np;
-  const bool st = p.stack;
-  const uint32_t plane = static_cast<uint32_t>(p.kpk) * NP * 128;  // bytes of one (hi or lo) operand
-  auto load_q = [&](int seg, float (&qv)[PER_KV][8]) {
-    const int g = seg % Hkv, b = seg / Hkv;
+  const int gid = warp * GPW + grp, ngroups = (kStreamThreads / 32) * GPW;
+  constexpr int UNR = QD_UNROLL;  // 8-row blocks in flight per group
+  for (int blk0 = gid; blk0 < nblk; blk0 += UNR * ngroups) {
+    uint4 rawb[UNR][8];
 #pragma unroll
-    for (int y = 0; y < PER_KV; ++y)
+    for (int ub = 0; ub < UNR; ++ub)
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        qv[y][e] = a.q[static_cast<long>(b) * a.q_stride + (g * PER_KV + y) * D + gl * 8 + e] * scale;
-  };
-  // Per-segment work, done by the block that owns the segment's first unit: the core's
-  // instance barrier reset, the tail append, the P image's zero padding and
-  // the appended row's logits.
-  for (long sg = nblk > 0 ? (u0 + nblk - 1) / nblk : u1; sg * nblk < u1; ++sg) {
-    const int seg = static_cast<int>(sg), g = seg % Hkv, b = seg / Hkv;
-    if (p.split && g == 0 && threadIdx.x == 0) a.ws_count[b] = 0u;  // core's per-instance barrier (after its wait)
-    unsigned char* pimg = a.ws_pimg + static_cast<size_t>(b) * 2 * plane;
-    if (a.append_kv) {  // the new token's k, v (this kv-head slice) -> tail row n_tail - 1
-      const float* src = a.q + static_cast<long>(b) * a.q_stride + static_cast<long>(H) * D + g * D;
-      const long row = static_cast<long>(b) * p.s.tail_cap + (n_tail - 1);
-      __nv_bfloat16* tk = const_cast<__nv_bfloat16*>(a.tail_k) + row * W + g * D;
-      __nv_bfloat16* tv = const_cast<__nv_bfloat16*>(a.tail_v) + row * W + g * D;
-      for (int i = threadIdx.x; i < D; i += kStreamThreads) {
-        tk[i] = __float2bfloat16_rn(src[i]);
-        tv[i] = __float2bfloat16_rn(src[W + i]);
+      for (int u = 0; u < 8; ++u) {
+        // unconditional load of a clamped row (no select right after the load, so
+        // all loads stay in flight); rows >= `rows` are discarded at emit
+        const int r = min((blk0 + ub * ngroups) * 8 + u, rows_ld - 1);
+        rawb[ub][u] = ldg_stream(r < rk ? rkb + static_cast<long>(r) * W : tkb + static_cast<long>(r - rk) * W);
       }
-      if (g == 0 && threadIdx.x == 0 && a.importance)
-        a.importance[static_cast<long>(b) * a.imp_stride + p.s.n_comp + n_tail - 1] = 0.0;
-      if (warp == 0) {  // its logits, from the fp32 source rounded to bf16 (both lane groups compute, group 0 writes)
-        float qv[PER_KV][8];
-        load_q(seg, qv);
-        float v[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] = __bfloat162float(__float2bfloat16_rn(src[gl * 8 + e]));
-        float* tout = a.ws_tail + static_cast<long>(b) * H * p.s.tail_cap;
-#pragma unroll
-        for (int y = 0; y < PER_KV; ++y) {
-          float t = v[0] * qv[y][0];
-#pragma unroll
-          for (int e = 1; e < 8; ++e) t = fmaf(v[e], qv[y][e], t);
-#pragma unroll
-          for (int o = LPH / 2; o >= 1; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-          if (lane == 0) tout[static_cast<long>(g * PER_KV + y) * p.s.tail_cap + (n_tail - 1)] = t;
-        }
-      }
-    }
-    // zero padding of the operand image: ranks >= rank_k of my heads; heads >= H (segment g == 0)
-    for (int i = threadIdx.x; i < PER_KV * (p.kpk * 64 - rk); i += kStreamThreads) {
-      const int h = g * PER_KV + i / (p.kpk * 64 - rk), r = rk + i % (p.kpk * 64 - rk);
-      *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(st, NP, p.kpk, r >> 6, h, r & 63, false)) = __float2bfloat16_rn(0.f);
-      *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(st, NP, p.kpk, r >> 6, h, r & 63, true)) = __float2bfloat16_rn(0.f);
-    }
-    if (g == 0)
-      for (int i = threadIdx.x; i < (NP - H) * p.kpk * 64; i += kStreamThreads) {
-        const int h = H + i / (p.kpk * 64), r = i % (p.kpk * 64);
-        *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(st, NP, p.kpk, r >> 6, h, r & 63, false)) = __float2bfloat16_rn(0.f);
-        *reinterpret_cast<__nv_bfloat16*>(pimg + bimg_off(st, NP, p.kpk, r >> 6, h, r & 63, true)) = __float2bfloat16_rn(0.f);
-      }
-  }
-  // Units of this block: warp w's groups take u0 + w*GPW + grp, then strides of all groups.  The loop runs
-  // while the warp's first group has a unit (shuffles stay warp-converged); a second group past u1 is masked.
-  const int ngroups = kStreamWarps * GPW;
-  int cur = -1;
-  float qv[PER_KV][8];
-  for (long uw = u0 + warp * GPW; uw < u1; uw += ngroups) {
-    const long u = uw + grp;
-    const bool live = u < u1;
-    const long uc = live ? u : uw;
-    const int seg = static_cast<int>(uc / nblk), blk = static_cast<int>(uc % nblk);
-    const int g = seg % Hkv, b = seg / Hkv;
-    const __nv_bfloat16* rkb = a.right_k + static_cast<long>(b) * rk * W + g * D + gl * 8;
-    const __nv_bfloat16* tkb = a.tail_k + static_cast<long>(b) * p.s.tail_cap * W + g * D + gl * 8;
-    uint4 raw[8];
-#pragma unroll
-    for (int u8 = 0; u8 < 8; ++u8) {
-      // unconditional load of a clamped row (no select right after the load, so
-      // all loads stay in flight); rows >= rows_ld are discarded at emit
-      const int r = min(blk * 8 + u8, rows_ld - 1);
-      raw[u8] = ldg_stream(r < rk ? rkb + static_cast<long>(r) * W : tkb + static_cast<long>(r - rk) * W);
-    }
-    if (seg != cur) {  // the query of this segment (L2-resident), loaded while the rows are in flight
-      load_q(seg, qv);
-      cur = seg;
-    }
-    unsigned char* pimg = a.ws_pimg + static_cast<size_t>(b) * 2 * plane;
-    float* tout = a.ws_tail + static_cast<long>(b) * H * p.s.tail_cap;
+    for (int ub = 0; ub < UNR; ++ub) {
+    const int blk = blk0 + ub * ngroups;
+    if (blk >= nblk) break;
     const int r0 = blk * 8;
+    const uint4* raw = rawb[ub];
 #pragma unroll
     for (int y = 0; y < PER_KV; ++y) {
       float acc[8];
 #pragma unroll
-      for (int u8 = 0; u8 < 8; ++u8) {
+      for (int u = 0; u < 8; ++u) {
         float v[8];
-        unpack8(raw[u8], v);
+        unpack8(raw[u], v);
         float t = v[0] * qv[y][0];
 #pragma unroll
         for (int e = 1; e < 8; ++e) t = fmaf(v[e], qv[y][e], t);
-        acc[u8] = t;
+        acc[u] = t;
       }
       // butterfly transpose-reduction of acc[0..7] across the LPH lanes of the group:
       // after the rounds, lane gl holds the full dot of row r0 + (gl % 8).
@@ -398,7 +365,7 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) qdots_kernel
       const int r = r0 + j;
       const int h = g * PER_KV + y;
       const bool owner = (gl < 8 * (LPH / 8)) && ((gl % (LPH / 8)) == 0);
-      if (live && owner && r < rows_ld) {
+      if (owner && r < rows_ld) {
         if (r < rk) {
           __nv_bfloat16 hi, lo;
           split_bf16(acc[0], hi, lo);
@@ -408,6 +375,22 @@ __global__ void __launch_bounds__(kStreamThreads, kStreamMinBlocks) qdots_kernel
           tout[static_cast<long>(h) * p.s.tail_cap + (r - rk)] = acc[0];
         }
       }
+    }
+    }
+  }
+  if (a.append_kv && gid == ngroups - 1) {  // the appended row (tail row n_tail - 1), one lane group
+    const float* src = a.q + static_cast<long>(b) * a.q_stride + static_cast<long>(H) * D + g * D + gl * 8;
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = __bfloat162float(__float2bfloat16_rn(src[e]));
+#pragma unroll
+    for (int y = 0; y < PER_KV; ++y) {
+      float t = v[0] * qv[y][0];
+#pragma unroll
+      for (int e = 1; e < 8; ++e) t = fmaf(v[e], qv[y][e], t);
+#pragma unroll
+      for (int o = LPH / 2; o >= 1; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      if (gl == 0) tout[static_cast<long>(g * PER_KV + y) * p.s.tail_cap + (n_tail - 1)] = t;
     }
   }
 }
@@ -1120,23 +1103,11 @@ int pdl_attr(cudaLaunchAttribute& at) {
   return 1;
 }
 
-int device_sms() {
-  static const int sms = [] {
-    int dev = 0, n = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n;
-  }();
-  return sms;
-}
-
 template <int PER_KV, int D>
 void launch_stream_pair(const FusedPlan& p, const FusedArgs& a, cudaStream_t st, bool first) {
   const dim3 grid(static_cast<unsigned>(p.s.Hkv), static_cast<unsigned>(p.s.batch));
-  // qdots: one wave of blocks over the flat unit list (units at the tail capacity bound the count)
-  const long units_max = static_cast<long>(p.s.Hkv) * p.s.batch * ((p.s.rank_k + p.s.tail_cap + 7) / 8);
-  const unsigned qblocks = static_cast<unsigned>(std::max(1L, std::min<long>(units_max, device_sms() * kStreamMinBlocks)));
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = first ? dim3(qblocks) : grid;
+  cfg.gridDim = grid;
   cfg.blockDim = dim3(kStreamThreads);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
